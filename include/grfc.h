@@ -1,0 +1,175 @@
+/*
+ * grfc — C-ABI of the B200-native Gaussian-random-field generator.
+ *
+ * This is the drop-in boundary for the reference's core generator
+ * (/root/reference/proj/core). Every entry point names the reference
+ * interface it replaces; the C++ drop-in (paper_1105_2737_b200/cpp, namespace
+ * grf) and the Python mirror (paper_1105_2737_b200/grfc.py) sit on top.
+ *
+ * Conventions (all from the reference code, which is authoritative over its
+ * SPEC/PAPER — SURVEY.md §A):
+ *   - grids are row-major, last index fastest (include/grf/grid.hpp:36);
+ *   - densities are evaluated at angular frequency w = 2 pi k~ / l with the
+ *     Nyquist index wrapping to +N/2 (src/grid.cpp:96-111);
+ *   - the field law is E[B B'] = (2 pi)^d/|A| sum_K g(w_K) cos(...)
+ *     (include/grf/synth.hpp:47-51).
+ *
+ * Pointers are plain; no torch/CUDA types cross the boundary (streams are
+ * passed as void* = cudaStream_t). All functions are thread-safe; a plan is
+ * immutable after creation (grfc_plan_set_sqrt_gamma_table must precede any
+ * generate call), and every call allocates its scratch stream-ordered, so one
+ * plan may serve concurrent calls on different streams.
+ */
+#ifndef GRFC_H
+#define GRFC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRFC_MAX_DIM 8
+
+typedef enum {
+  GRFC_OK = 0,
+  GRFC_EINVAL = 1,   /* reference: std::invalid_argument */
+  GRFC_ERUNTIME = 2, /* reference: std::runtime_error (NaN density, exhaustion) */
+  GRFC_ECUDA = 3,    /* CUDA runtime failure (no reference analogue) */
+  GRFC_ENCCL = 4     /* collective failure (slab path) */
+} grfc_status;
+
+typedef enum { GRFC_F32 = 0, GRFC_F64 = 1 } grfc_dtype;
+
+/* Same order as grf::Algorithm (include/grf/synth.hpp:18-25). */
+typedef enum {
+  GRFC_TWO_FFT = 0,
+  GRFC_ONE_FFT_OVERWRITE = 1,
+  GRFC_ONE_FFT_RECURSIVE = 2
+} grfc_algorithm;
+
+/* Spectral-density descriptor: the POD image of a grf::SpectralDensity
+ * (include/grf/spectral.hpp:14-85) that the device can evaluate in-kernel.
+ *   POLY     r[0]=m, i[0]=k, i[1]=l, i[2]=n        (spectral.cpp:42-55)
+ *   ANISO    r[0]=m, i[0]=n, i[1+a]=k_a            (spectral.cpp:65-78)
+ *   TEST1D   -                                     (spectral.cpp:88-93)
+ *   GAUSSIAN_COV r[0]=ell: (ell/sqrt(2pi))^d exp(-ell^2|w|^2/2)
+ *   MATERN   r[0]=nu, r[1]=ell: c (1+ell^2|w|^2)^-(nu+d/2),
+ *            c = ell^d Gamma(nu+d/2)/(pi^{d/2} Gamma(nu))
+ *   CONSTANT r[0]=c
+ *   TABLE    any user density: sqrt(g) supplied per half-lattice cell by
+ *            grfc_plan_set_sqrt_gamma_table (host-evaluated, NaN-checked). */
+typedef enum {
+  GRFC_DENSITY_POLY = 0,
+  GRFC_DENSITY_ANISO = 1,
+  GRFC_DENSITY_TEST1D = 2,
+  GRFC_DENSITY_GAUSSIAN_COV = 3,
+  GRFC_DENSITY_MATERN = 4,
+  GRFC_DENSITY_CONSTANT = 5,
+  GRFC_DENSITY_TABLE = 6
+} grfc_density_family;
+
+typedef struct {
+  int family;
+  int dim;
+  double r[8];
+  int i[8];
+} grfc_density;
+
+typedef struct grfc_plan_s* grfc_plan;
+
+/* Last error message of the calling thread ("" if none). */
+const char* grfc_last_error(void);
+
+/* Exact number of N(0,1) draws one field consumes.
+ * Replaces grf::count_draws (src/synth.cpp:211-218) and
+ * grf::spectrum_draw_count (src/hermitian.cpp:228-236). */
+grfc_status grfc_count_draws(int dim, const int64_t* counts, int algorithm, uint64_t* out);
+
+/* Half-lattice size |H| = N_1..N_{d-1} (N_d/2+1): the length of the table
+ * grfc_plan_set_sqrt_gamma_table expects (row-major over H). */
+grfc_status grfc_half_lattice_cells(int dim, const int64_t* counts, uint64_t* out);
+
+/* Plan = GridSpec (include/grf/grid.hpp:16-47, validated as src/grid.cpp:10-30)
+ * + density + algorithm + precision, bound to one device. Replaces the
+ * per-call setup of grf::synthesize (src/synth.cpp:68-80) and the FFTW plan
+ * cache (src/dft.cpp:27-69). */
+grfc_status grfc_plan_create(grfc_plan* plan, int dim, const int64_t* counts,
+                             const double* lengths, int dtype, int algorithm,
+                             const grfc_density* density, int device);
+/* sqrt(g(w_K)) for every K of the half-lattice H, row-major; required for
+ * GRFC_DENSITY_TABLE (user SpectralDensity subclasses). Rejects NaN/negative
+ * with GRFC_ERUNTIME like src/hermitian.cpp:147-148. */
+grfc_status grfc_plan_set_sqrt_gamma_table(grfc_plan plan, const double* sqrt_gamma);
+void grfc_plan_destroy(grfc_plan plan);
+
+/* Seeded batch generation — the device form of
+ * grf::synthesize(grid, density, seed, algorithm) (src/synth.cpp:129-135),
+ * extended to a batch the way the reference's stats.cpp:105 derives
+ * substreams (seed, j). Field f (f = first_field .. first_field+nfields-1) is
+ * a pure function of (seed, f): Philox4x32-10 keyed by seed, counter
+ * (cell, f). Output: nfields fields of P elements (dtype), field i at
+ * d_out + i*field_stride elements. Asynchronous on `stream`. */
+grfc_status grfc_generate(grfc_plan plan, uint64_t seed, uint64_t first_field, uint64_t nfields,
+                          void* d_out, uint64_t field_stride, void* stream);
+
+/* Same as grfc_generate but writes to HOST memory (pinned or pageable):
+ * generation of chunk i+1 overlaps the D2H copy of chunk i. Synchronous.
+ * This is the end-to-end form of grf::synthesize returning RealField.values. */
+grfc_status grfc_generate_host(grfc_plan plan, uint64_t seed, uint64_t first_field,
+                               uint64_t nfields, void* h_out, void* stream);
+
+/* Injected-noise synthesis of one field: `draws` are the N(0,1) values in
+ * the reference's own draw order (exactly count_draws of them) — i.e. what
+ * grf::synthesize(grid, density, GaussianStream&, algorithm)
+ * (src/synth.cpp:68-127) would pull from a FixedStream. The Hermitian
+ * arrangement of src/hermitian.cpp:128-203 is resolved on the host; FFTs run
+ * on device. This is the parity path and the stream-overload drop-in. */
+grfc_status grfc_generate_injected(grfc_plan plan, const double* draws, uint64_t ndraws,
+                                   void* d_out, void* stream);
+
+/* Host-only noise bridge (no device): the unit-variance Hermitian noise w(K)
+ * the reference would assemble from `draws` (its own draw order) for every
+ * half-lattice cell K, row-major over H, interleaved (re, im) — i.e. the
+ * spectrum of src/hermitian.cpp:128-203 divided by sqrt(g). w_half holds
+ * 2*|H| doubles. algorithm must be ONE_FFT_OVERWRITE or ONE_FFT_RECURSIVE. */
+grfc_status grfc_half_noise_from_draws(int dim, const int64_t* counts, int algorithm, const double* draws,
+                                       uint64_t ndraws, double* w_half);
+
+/* The Philox noise grfc_generate uses for field (seed, field), in the
+ * reference's draw order (count_draws values, as doubles; fp32 plans give
+ * fp32-valued noise). Feeding it to the reference through a FixedStream
+ * reproduces grfc_generate's field. Synchronous. */
+grfc_status grfc_dump_noise(grfc_plan plan, uint64_t seed, uint64_t field, double* draws,
+                            uint64_t ndraws);
+
+/* Device complex DFT with the reference DftBackend contract
+ * (include/grf/dft.hpp:11-25): sign=+1 "forward" out[K] = sum in[J] e^{+...};
+ * sign=-1 "inverse" out[J] = P^-1 sum in[K] e^{-...}. fp64 interleaved,
+ * device pointers, out-of-place (in == out rejected as src/dft.cpp:21-22). */
+grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, double* d_out,
+                         int sign, void* stream);
+
+/* Plan introspection for benchmarks: bytes of workspace per field and the
+ * kernel path chosen ("pow2-2d", "generic", ...). */
+grfc_status grfc_plan_info(grfc_plan plan, uint64_t* cells_half, uint64_t* points,
+                           const char** path);
+
+/* Number of kernel launches the last generate call on this thread issued. */
+uint64_t grfc_last_launch_count(void);
+
+/* Per-kernel timing for benchmarks, per calling thread: while enabled, every
+ * kernel the library launches is bracketed by CUDA events recorded on the
+ * stream it is launched on. Enabling clears previous records. */
+void grfc_kernel_timing_enable(int on);
+/* Records aggregated by kernel name (synchronises the events): the index-th
+ * kernel's name, summed device milliseconds and launch count. GRFC_EINVAL
+ * past the last kernel. */
+grfc_status grfc_kernel_timing_read(int index, const char** name, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,616 @@
+// grfc C-ABI: plans, dispatch, the host<->device boundary and error mapping.
+// See include/grfc.h for the contract and the reference interfaces replaced.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/grfc.h"
+#include "fast2d.h"
+#include "grfc_internal.cuh"
+#include "host_lattice.h"
+#include "kernels.h"
+
+namespace grfc {
+
+static thread_local std::string t_err;
+static thread_local uint64_t t_launches = 0;
+void count_launch(uint64_t n) { t_launches += n; }
+
+// ---- per-kernel timing (benchmarks)
+struct TimedLaunch {
+  const char* name;
+  cudaEvent_t start, stop;
+};
+static thread_local bool t_timing = false;
+static thread_local std::vector<TimedLaunch> t_timed;
+struct TimingRow {
+  std::string name;
+  double ms = 0;
+  uint64_t launches = 0;
+};
+static thread_local std::vector<TimingRow> t_rows;
+
+LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s) {
+  if (t_timing) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    start = (void*)e;
+  }
+}
+
+LaunchScope::~LaunchScope() {
+  count_launch();
+  if (start) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    t_timed.push_back({name, (cudaEvent_t)start, e});
+  }
+}
+
+static grfc_status fail(grfc_status s, const std::string& msg) {
+  t_err = msg;
+  return s;
+}
+
+#define GRFC_CUDA(expr)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: ") + #expr + ": " + \
+                                                       cudaGetErrorString(e_));          \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+Factors factorize(int64_t n) {
+  Factors F{};
+  int64_t m = n;
+  while (m % 8 == 0 && F.nf < 40) F.r[F.nf++] = 8, m /= 8;
+  while (m % 4 == 0) F.r[F.nf++] = 4, m /= 4;
+  while (m % 2 == 0) F.r[F.nf++] = 2, m /= 2;
+  for (int64_t p = 3; m > 1; p += 2) {
+    while (m % p == 0) F.r[F.nf++] = (int)p, m /= p;
+    if (p * p > m && m > 1) F.r[F.nf++] = (int)m, m = 1;
+  }
+  return F;
+}
+
+// exp(+2 pi i m / n), m < n, from long-double angles (one rounding to T).
+template <typename T>
+static std::vector<C_t<T>> twiddle_table(int64_t n) {
+  std::vector<C_t<T>> t((size_t)n);
+  const long double two_pi = 6.283185307179586476925286766559L;
+  for (int64_t m = 0; m < n; ++m) {
+    const long double a = two_pi * (long double)m / (long double)n;
+    t[(size_t)m].x = (T)cosl(a);
+    t[(size_t)m].y = (T)sinl(a);
+  }
+  return t;
+}
+
+static double two_pi_pow(int d) {  // src/synth.cpp:13-17
+  double v = 1.0;
+  for (int i = 0; i < d; ++i) v *= 2.0 * M_PI;
+  return v;
+}
+
+}  // namespace grfc
+
+using namespace grfc;
+
+struct grfc_plan_s {
+  int d = 0;
+  int64_t n[GRFC_MAX_DIM] = {};
+  double l[GRFC_MAX_DIM] = {};
+  int dtype = GRFC_F32, alg = 1, device = 0;
+  grfc_density dens{};
+  GridDesc g{};
+  DensityDesc D{};
+  uint64_t cells = 0, points = 0;
+  size_t csize = 8;  // bytes per complex element
+  void* d_tw = nullptr;
+  size_t tw_off[GRFC_MAX_DIM] = {};  // element offsets per axis
+  Factors F[GRFC_MAX_DIM]{};
+  Factors FM{};  // last axis: factors of n_d / 2
+  double* d_table = nullptr;
+  bool table_set = false;
+  double s_one = 1.0;  // Alg 2/3: sqrt((2 pi)^d / |A|)         (synth.cpp:123)
+  double s_two = 1.0;  // Alg 1:   sqrt((2 pi)^d P / |A|) / P   (synth.cpp:89-90 + dft.cpp:106)
+  bool fast = false;
+  Fast2D fast2d{};
+  std::string path = "generic";
+
+  const void* tw(int a) const { return (const char*)d_tw + tw_off[a] * csize; }
+};
+
+namespace grfc {
+
+static grfc_status validate_density(const grfc_density* dn, int d) {
+  if (!dn) return fail(GRFC_EINVAL, "grfc: density is null");
+  if (dn->dim != d) return fail(GRFC_EINVAL, "synthesize: density dimension mismatch");
+  switch (dn->family) {
+    case GRFC_DENSITY_POLY:
+      if (!(dn->r[0] > 0.0) || !std::isfinite(dn->r[0]))
+        return fail(GRFC_EINVAL, "PolyDecayDensity: m must be positive");
+      if (dn->i[0] < 1 || dn->i[1] < 1 || dn->i[2] < 1)
+        return fail(GRFC_EINVAL, "PolyDecayDensity: k, l, n must be >= 1");
+      return GRFC_OK;
+    case GRFC_DENSITY_ANISO:
+      if (!(dn->r[0] > 0.0) || !std::isfinite(dn->r[0]))
+        return fail(GRFC_EINVAL, "AnisoPolyDensity: m must be positive");
+      if (dn->i[0] < 1) return fail(GRFC_EINVAL, "AnisoPolyDensity: n must be >= 1");
+      for (int a = 0; a < d; ++a)
+        if (dn->i[1 + a] < 1) return fail(GRFC_EINVAL, "AnisoPolyDensity: exponents must be >= 1");
+      return GRFC_OK;
+    case GRFC_DENSITY_TEST1D:
+      if (d != 1) return fail(GRFC_EINVAL, "density spec: test1d is one-dimensional");
+      return GRFC_OK;
+    case GRFC_DENSITY_GAUSSIAN_COV:
+      if (!(dn->r[0] > 0.0) || !std::isfinite(dn->r[0])) return fail(GRFC_EINVAL, "gaussian-cov: ell must be > 0");
+      return GRFC_OK;
+    case GRFC_DENSITY_MATERN:
+      if (!(dn->r[0] > 0.0) || !std::isfinite(dn->r[0])) return fail(GRFC_EINVAL, "matern: nu must be > 0");
+      if (!(dn->r[1] > 0.0) || !std::isfinite(dn->r[1])) return fail(GRFC_EINVAL, "matern: ell must be > 0");
+      return GRFC_OK;
+    case GRFC_DENSITY_CONSTANT:
+      if (!(dn->r[0] >= 0.0) || std::isnan(dn->r[0]))
+        return fail(GRFC_ERUNTIME, "synthesize_spectrum: density evaluated to NaN or negative");
+      return GRFC_OK;
+    case GRFC_DENSITY_TABLE: return GRFC_OK;
+  }
+  return fail(GRFC_EINVAL, "grfc: unknown density family");
+}
+
+template <typename T>
+static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
+                              int64_t stride, const double2* inj_half, const double* inj_points, cudaStream_t s) {
+  const int d = p->d;
+  const int nd = (int)p->n[d - 1];
+  const int64_t rows_pf = (int64_t)(p->points / (uint64_t)nd);
+  const int64_t rows = rows_pf * nf;
+  if (p->fast && !inj_half && !inj_points) {
+    GRFC_CUDA(launch_fast2d(p->fast2d, p->alg, seed, field0, nf, W, out, stride, s));
+    return GRFC_OK;
+  }
+  auto axes = [&](int sign) -> grfc_status {
+    for (int a = 0; a < d - 1; ++a) {
+      int64_t inner = p->n[d - 1] / 2 + 1, outer = nf;
+      for (int b = a + 1; b < d - 1; ++b) inner *= p->n[b];
+      for (int b = 0; b < a; ++b) outer *= p->n[b];
+      cudaError_t e = launch_line_c2c<T>(W, (int)p->n[a], inner, outer, sign, p->F[a], p->tw(a), s);
+      if (e == cudaErrorInvalidValue)
+        return fail(GRFC_EINVAL, "grfc: axis length " + std::to_string(p->n[a]) + " exceeds the on-chip line limit");
+      GRFC_CUDA(e);
+    }
+    return GRFC_OK;
+  };
+  grfc_status st;
+  if (p->alg == GRFC_TWO_FFT) {
+    cudaError_t e = launch_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, p->FM, p->tw(d - 1), s);
+    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: last-axis length exceeds the on-chip line limit");
+    GRFC_CUDA(e);
+    if ((st = axes(+1)) != GRFC_OK) return st;
+    GRFC_CUDA(launch_scale_half<T>(p->g, p->D, p->s_two, W, nf, s));
+    if ((st = axes(-1)) != GRFC_OK) return st;
+    GRFC_CUDA(launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, p->FM, p->tw(d - 1), s));
+  } else {
+    GRFC_CUDA(launch_gen_half<T>(p->g, p->D, p->alg, p->s_one, seed, field0, inj_half, W, nf, s));
+    if ((st = axes(+1)) != GRFC_OK) return st;
+    cudaError_t e = launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, p->FM, p->tw(d - 1), s);
+    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: last-axis length exceeds the on-chip line limit");
+    GRFC_CUDA(e);
+  }
+  return GRFC_OK;
+}
+
+static grfc_status run_fields_any(grfc_plan p, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
+                                  int64_t stride, const double2* inj_half, const double* inj_points,
+                                  cudaStream_t s) {
+  if (p->dtype == GRFC_F64) return run_fields<double>(p, seed, field0, nf, W, out, stride, inj_half, inj_points, s);
+  return run_fields<float>(p, seed, field0, nf, W, out, stride, inj_half, inj_points, s);
+}
+
+// Fields per workspace chunk: keep the half-spectrum intermediate L2-resident.
+static int64_t chunk_fields(grfc_plan p, uint64_t nfields) {
+  const double wbytes = (double)p->cells * (double)p->csize;
+  int64_t c = (int64_t)std::floor((p->fast ? p->fast2d.l2_budget : 48.0 * 1024 * 1024) / wbytes);
+  c = std::max<int64_t>(1, std::min<int64_t>(c, (int64_t)nfields));
+  return c;
+}
+
+static size_t dsize(grfc_plan p) { return p->dtype == GRFC_F64 ? 8 : 4; }
+
+}  // namespace grfc
+
+extern "C" {
+
+const char* grfc_last_error(void) { return t_err.c_str(); }
+uint64_t grfc_last_launch_count(void) { return t_launches; }
+
+void grfc_kernel_timing_enable(int on) {
+  for (auto& t : t_timed) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  t_timed.clear();
+  t_rows.clear();
+  t_timing = on != 0;
+}
+
+grfc_status grfc_kernel_timing_read(int index, const char** name, double* total_ms, uint64_t* launches) {
+  for (auto& t : t_timed) {
+    cudaEventSynchronize(t.stop);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.start, t.stop);
+    auto it = std::find_if(t_rows.begin(), t_rows.end(), [&](const TimingRow& r) { return r.name == t.name; });
+    if (it == t_rows.end()) {
+      t_rows.push_back({t.name, 0.0, 0});
+      it = t_rows.end() - 1;
+    }
+    it->ms += ms;
+    it->launches += 1;
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  t_timed.clear();
+  if (index < 0 || index >= (int)t_rows.size()) return fail(GRFC_EINVAL, "grfc: no such timing row");
+  if (name) *name = t_rows[(size_t)index].name.c_str();
+  if (total_ms) *total_ms = t_rows[(size_t)index].ms;
+  if (launches) *launches = t_rows[(size_t)index].launches;
+  return GRFC_OK;
+}
+
+grfc_status grfc_count_draws(int dim, const int64_t* counts, int algorithm, uint64_t* out) {
+  std::string err;
+  if (!counts || !out) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!validate_grid(dim, counts, nullptr, err)) return fail(GRFC_EINVAL, err);
+  if (algorithm < 0 || algorithm > 2) return fail(GRFC_EINVAL, "count_draws: unknown algorithm");
+  *out = grfc::count_draws(dim, counts, algorithm);
+  return GRFC_OK;
+}
+
+grfc_status grfc_half_lattice_cells(int dim, const int64_t* counts, uint64_t* out) {
+  std::string err;
+  if (!counts || !out) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!validate_grid(dim, counts, nullptr, err)) return fail(GRFC_EINVAL, err);
+  *out = half_cells(dim, counts);
+  return GRFC_OK;
+}
+
+grfc_status grfc_half_noise_from_draws(int dim, const int64_t* counts, int algorithm, const double* draws,
+                                       uint64_t ndraws, double* w_half) {
+  std::string err;
+  if (!counts || !w_half || (!draws && ndraws)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!validate_grid(dim, counts, nullptr, err)) return fail(GRFC_EINVAL, err);
+  if (algorithm != GRFC_ONE_FFT_OVERWRITE && algorithm != GRFC_ONE_FFT_RECURSIVE)
+    return fail(GRFC_EINVAL, "grfc: half-lattice noise exists for the one-FFT algorithms only");
+  std::vector<double> w;
+  if (!arrange_half_noise(dim, counts, algorithm, draws, ndraws, w, err)) return fail(GRFC_ERUNTIME, err);
+  std::memcpy(w_half, w.data(), w.size() * sizeof(double));
+  return GRFC_OK;
+}
+
+grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, const double* lengths, int dtype,
+                             int algorithm, const grfc_density* density, int device) {
+  if (!out || !counts || !lengths) return fail(GRFC_EINVAL, "grfc: null argument");
+  *out = nullptr;
+  std::string err;
+  if (!validate_grid(dim, counts, lengths, err)) return fail(GRFC_EINVAL, err);
+  if (dtype != GRFC_F32 && dtype != GRFC_F64) return fail(GRFC_EINVAL, "grfc: dtype must be F32 or F64");
+  if (algorithm < 0 || algorithm > 2) return fail(GRFC_EINVAL, "synthesize: unknown algorithm");
+  grfc_status st = validate_density(density, dim);
+  if (st != GRFC_OK) return st;
+  int ndev = 0;
+  GRFC_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(GRFC_EINVAL, "grfc: bad device ordinal");
+  DeviceGuard guard(device);
+
+  std::unique_ptr<grfc_plan_s> p(new grfc_plan_s());
+  p->d = dim;
+  p->dtype = dtype;
+  p->alg = algorithm;
+  p->device = device;
+  p->dens = *density;
+  p->csize = dtype == GRFC_F64 ? 16 : 8;
+  p->points = 1;
+  double vol = 1.0;
+  for (int a = 0; a < dim; ++a) {
+    p->n[a] = counts[a];
+    p->l[a] = lengths[a];
+    p->points *= (uint64_t)counts[a];
+    vol *= lengths[a];
+  }
+  p->cells = half_cells(dim, counts);
+  // GridDesc
+  p->g.d = dim;
+  for (int a = 0; a < dim; ++a) {
+    p->g.n[a] = counts[a];
+    p->g.l[a] = lengths[a];
+    p->g.w_of_k[a] = 2.0 * M_PI / lengths[a];
+  }
+  p->g.hd = counts[dim - 1] / 2 + 1;
+  p->g.cells = (int64_t)p->cells;
+  p->g.points = (int64_t)p->points;
+  // DensityDesc
+  DensityDesc& D = p->D;
+  D.family = density->family;
+  D.d = dim;
+  std::memcpy(D.r, density->r, sizeof D.r);
+  std::memcpy(D.i, density->i, sizeof D.i);
+  if (D.family == GRFC_DENSITY_GAUSSIAN_COV) {
+    D.sqrt_c = std::sqrt(std::pow(D.r[0] / std::sqrt(2.0 * M_PI), dim));
+  } else if (D.family == GRFC_DENSITY_MATERN) {
+    const double nu = D.r[0], ell = D.r[1];
+    D.alpha = nu + 0.5 * dim;
+    D.sqrt_c = std::sqrt(std::pow(ell, dim) * std::tgamma(D.alpha) / (std::pow(M_PI, 0.5 * dim) * std::tgamma(nu)));
+  } else if (D.family == GRFC_DENSITY_POLY) {
+    D.mkl = std::pow(D.r[0], (double)D.i[0] * (double)D.i[1]);
+  }
+  p->s_one = std::sqrt(two_pi_pow(dim) / vol);
+  p->s_two = std::sqrt(two_pi_pow(dim) * (double)p->points / vol) / (double)p->points;
+
+  // Twiddle tables: one per axis length.
+  size_t total = 0;
+  for (int a = 0; a < dim; ++a) {
+    p->tw_off[a] = total;
+    total += (size_t)counts[a];
+    p->F[a] = factorize(counts[a]);
+  }
+  p->FM = factorize(counts[dim - 1] / 2);
+  GRFC_CUDA(cudaMalloc(&p->d_tw, total * p->csize));
+  for (int a = 0; a < dim; ++a) {
+    if (dtype == GRFC_F64) {
+      auto t = twiddle_table<double>(counts[a]);
+      GRFC_CUDA(cudaMemcpy((char*)p->d_tw + p->tw_off[a] * p->csize, t.data(), t.size() * p->csize,
+                           cudaMemcpyHostToDevice));
+    } else {
+      auto t = twiddle_table<float>(counts[a]);
+      GRFC_CUDA(cudaMemcpy((char*)p->d_tw + p->tw_off[a] * p->csize, t.data(), t.size() * p->csize,
+                           cudaMemcpyHostToDevice));
+    }
+  }
+  if (density->family == GRFC_DENSITY_TABLE) GRFC_CUDA(cudaMalloc(&p->d_table, p->cells * sizeof(double)));
+  // Fused fast path for power-of-two 2D shapes (pow2_2d.cu).
+  if (density->family != GRFC_DENSITY_TABLE && fast2d_supported(dim, counts, dtype, algorithm, density->family)) {
+    GRFC_CUDA(fast2d_init(p->fast2d, p->g, p->D, dtype, algorithm, p->s_one, p->s_two));
+    p->fast = true;
+    p->path = fast2d_name(p->fast2d);
+  }
+  *out = p.release();
+  return GRFC_OK;
+}
+
+grfc_status grfc_plan_set_sqrt_gamma_table(grfc_plan p, const double* sg) {
+  if (!p || !sg) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (p->dens.family != GRFC_DENSITY_TABLE) return fail(GRFC_EINVAL, "grfc: plan density is not a table");
+  for (uint64_t h = 0; h < p->cells; ++h)
+    if (!(sg[h] >= 0.0) || std::isnan(sg[h]))
+      return fail(GRFC_ERUNTIME, "synthesize_spectrum: density evaluated to NaN or negative");
+  DeviceGuard guard(p->device);
+  GRFC_CUDA(cudaMemcpy(p->d_table, sg, p->cells * sizeof(double), cudaMemcpyHostToDevice));
+  p->D.table = p->d_table;
+  p->table_set = true;
+  return GRFC_OK;
+}
+
+void grfc_plan_destroy(grfc_plan p) {
+  if (!p) return;
+  DeviceGuard guard(p->device);
+  if (p->fast) fast2d_free(p->fast2d);
+  cudaFree(p->d_tw);
+  cudaFree(p->d_table);
+  delete p;
+}
+
+grfc_status grfc_plan_info(grfc_plan p, uint64_t* cells, uint64_t* points, const char** path) {
+  if (!p) return fail(GRFC_EINVAL, "grfc: null plan");
+  if (cells) *cells = p->cells;
+  if (points) *points = p->points;
+  if (path) *path = p->path.c_str();
+  return GRFC_OK;
+}
+
+grfc_status grfc_generate(grfc_plan p, uint64_t seed, uint64_t first_field, uint64_t nfields, void* d_out,
+                          uint64_t field_stride, void* stream) {
+  t_launches = 0;
+  if (!p || (!d_out && nfields)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (p->dens.family == GRFC_DENSITY_TABLE && !p->table_set)
+    return fail(GRFC_EINVAL, "grfc: sqrt-gamma table not set");
+  if (field_stride < p->points && nfields > 1) return fail(GRFC_EINVAL, "grfc: field_stride < point count");
+  if (nfields == 0) return GRFC_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t chunk = chunk_fields(p, nfields);
+  void* W = nullptr;
+  GRFC_CUDA(cudaMallocAsync(&W, (size_t)chunk * p->cells * p->csize, s));
+  grfc_status st = GRFC_OK;
+  for (uint64_t f = 0; f < nfields && st == GRFC_OK; f += (uint64_t)chunk) {
+    const int64_t nf = (int64_t)std::min<uint64_t>((uint64_t)chunk, nfields - f);
+    st = run_fields_any(p, seed, first_field + f, nf, W, (char*)d_out + f * field_stride * dsize(p),
+                        (int64_t)field_stride, nullptr, nullptr, s);
+  }
+  cudaFreeAsync(W, s);
+  return st;
+}
+
+grfc_status grfc_generate_host(grfc_plan p, uint64_t seed, uint64_t first_field, uint64_t nfields, void* h_out,
+                               void* stream) {
+  t_launches = 0;
+  if (!p || (!h_out && nfields)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (nfields == 0) return GRFC_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t sg = (cudaStream_t)stream;
+  const size_t fbytes = p->points * dsize(p);
+  // Output chunks of ~64 MiB, double-buffered against the D2H copies.
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>((int64_t)nfields, (int64_t)((64u << 20) / fbytes)));
+  cudaStream_t sc;
+  GRFC_CUDA(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+  cudaEvent_t gen[2], cp[2];
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&gen[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&cp[i], cudaEventDisableTiming);
+  }
+  void* buf[2] = {nullptr, nullptr};
+  grfc_status st = GRFC_OK;
+  cudaError_t e = cudaMallocAsync(&buf[0], (size_t)chunk * fbytes, sg);
+  if (e == cudaSuccess) e = cudaMallocAsync(&buf[1], (size_t)chunk * fbytes, sg);
+  if (e != cudaSuccess) st = fail(GRFC_ECUDA, std::string("CUDA: cudaMallocAsync: ") + cudaGetErrorString(e));
+  uint64_t launches = 0;
+  int i = 0;
+  for (uint64_t f = 0; f < nfields && st == GRFC_OK; f += (uint64_t)chunk, ++i) {
+    const int b = i & 1;
+    const int64_t nf = (int64_t)std::min<uint64_t>((uint64_t)chunk, nfields - f);
+    if (i >= 2) cudaStreamWaitEvent(sg, cp[b], 0);
+    st = grfc_generate(p, seed, first_field + f, (uint64_t)nf, buf[b], p->points, sg);
+    launches += t_launches;
+    if (st != GRFC_OK) break;
+    cudaEventRecord(gen[b], sg);
+    cudaStreamWaitEvent(sc, gen[b], 0);
+    e = cudaMemcpyAsync((char*)h_out + f * fbytes, buf[b], (size_t)nf * fbytes, cudaMemcpyDeviceToHost, sc);
+    if (e != cudaSuccess) st = fail(GRFC_ECUDA, std::string("CUDA: D2H: ") + cudaGetErrorString(e));
+    cudaEventRecord(cp[b], sc);
+  }
+  cudaStreamSynchronize(sc);
+  cudaStreamWaitEvent(sg, cp[0], 0);
+  cudaStreamWaitEvent(sg, cp[1], 0);
+  if (buf[0]) cudaFreeAsync(buf[0], sg);
+  if (buf[1]) cudaFreeAsync(buf[1], sg);
+  e = cudaStreamSynchronize(sg);
+  if (e != cudaSuccess && st == GRFC_OK) st = fail(GRFC_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e));
+  for (int j = 0; j < 2; ++j) {
+    cudaEventDestroy(gen[j]);
+    cudaEventDestroy(cp[j]);
+  }
+  cudaStreamDestroy(sc);
+  t_launches = launches;
+  return st;
+}
+
+grfc_status grfc_generate_injected(grfc_plan p, const double* draws, uint64_t ndraws, void* d_out, void* stream) {
+  t_launches = 0;
+  if (!p || !d_out || (!draws && ndraws)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (p->dens.family == GRFC_DENSITY_TABLE && !p->table_set)
+    return fail(GRFC_EINVAL, "grfc: sqrt-gamma table not set");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<double> host;
+  const double* src = nullptr;
+  size_t nbytes = 0;
+  if (p->alg == GRFC_TWO_FFT) {
+    if (ndraws < p->points) return fail(GRFC_ERUNTIME, "FixedStream: stream exhausted");
+    src = draws;
+    nbytes = p->points * sizeof(double);
+  } else {
+    std::string err;
+    if (!arrange_half_noise(p->d, p->n, p->alg, draws, ndraws, host, err)) return fail(GRFC_ERUNTIME, err);
+    src = host.data();
+    nbytes = host.size() * sizeof(double);
+  }
+  void* dnoise = nullptr;
+  void* W = nullptr;
+  GRFC_CUDA(cudaMallocAsync(&dnoise, nbytes, s));
+  GRFC_CUDA(cudaMallocAsync(&W, p->cells * p->csize, s));
+  GRFC_CUDA(cudaMemcpyAsync(dnoise, src, nbytes, cudaMemcpyHostToDevice, s));
+  grfc_status st = run_fields_any(p, 0, 0, 1, W, d_out, (int64_t)p->points,
+                                  p->alg == GRFC_TWO_FFT ? nullptr : (const double2*)dnoise,
+                                  p->alg == GRFC_TWO_FFT ? (const double*)dnoise : nullptr, s);
+  cudaFreeAsync(W, s);
+  cudaFreeAsync(dnoise, s);
+  // `host` is pageable: cudaMemcpyAsync from it completed before returning.
+  if (st == GRFC_OK) GRFC_CUDA(cudaStreamSynchronize(s));
+  return st;
+}
+
+grfc_status grfc_dump_noise(grfc_plan p, uint64_t seed, uint64_t field, double* draws, uint64_t ndraws) {
+  t_launches = 0;
+  if (!p || !draws) return fail(GRFC_EINVAL, "grfc: null argument");
+  const uint64_t need = grfc::count_draws(p->d, p->n, p->alg);
+  if (ndraws < need) return fail(GRFC_EINVAL, "grfc: draws buffer shorter than count_draws");
+  DeviceGuard guard(p->device);
+  std::vector<uint64_t> ctr;
+  std::vector<uint8_t> nd;
+  reference_order_counters(p->d, p->n, p->alg, ctr, nd);
+  uint64_t* dctr = nullptr;
+  double* dpairs = nullptr;
+  GRFC_CUDA(cudaMalloc(&dctr, ctr.size() * sizeof(uint64_t)));
+  GRFC_CUDA(cudaMalloc(&dpairs, ctr.size() * 2 * sizeof(double)));
+  GRFC_CUDA(cudaMemcpy(dctr, ctr.data(), ctr.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  cudaError_t e = p->dtype == GRFC_F64 ? launch_philox_pairs<double>(dctr, (int64_t)ctr.size(), seed, field, dpairs, 0)
+                                       : launch_philox_pairs<float>(dctr, (int64_t)ctr.size(), seed, field, dpairs, 0);
+  std::vector<double> pairs(ctr.size() * 2);
+  if (e == cudaSuccess) e = cudaMemcpy(pairs.data(), dpairs, pairs.size() * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(dctr);
+  cudaFree(dpairs);
+  if (e != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: dump: ") + cudaGetErrorString(e));
+  uint64_t pos = 0;
+  for (size_t i = 0; i < ctr.size(); ++i) {
+    draws[pos++] = pairs[2 * i];
+    if (nd[i] == 2) draws[pos++] = pairs[2 * i + 1];
+  }
+  return GRFC_OK;
+}
+
+grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, double* d_out, int sign, void* stream) {
+  t_launches = 0;
+  if (!counts || !d_in || !d_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (d_in == d_out) return fail(GRFC_EINVAL, "DftBackend: in-place transform not supported");
+  if (dim < 1 || dim > GRFC_MAX_DIM) return fail(GRFC_EINVAL, "grfc: bad dimension");
+  int64_t P = 1;
+  for (int a = 0; a < dim; ++a) {
+    if (counts[a] < 1) return fail(GRFC_EINVAL, "grfc: bad extent");
+    P *= counts[a];
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // Per-length twiddle tables, cached per device for the process lifetime.
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, void*> cache;
+  int dev = 0;
+  GRFC_CUDA(cudaGetDevice(&dev));
+  GRFC_CUDA(cudaMemcpyAsync(d_out, d_in, (size_t)P * 16, cudaMemcpyDeviceToDevice, s));
+  for (int a = 0; a < dim; ++a) {
+    const int64_t n = counts[a];
+    if (n == 1) continue;
+    void* tw = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = cache.find({dev, n});
+      if (it == cache.end()) {
+        auto t = twiddle_table<double>(n);
+        GRFC_CUDA(cudaMalloc(&tw, t.size() * 16));
+        GRFC_CUDA(cudaMemcpy(tw, t.data(), t.size() * 16, cudaMemcpyHostToDevice));
+        cache[{dev, n}] = tw;
+      } else {
+        tw = it->second;
+      }
+    }
+    int64_t inner = 1, outer = 1;
+    for (int b = a + 1; b < dim; ++b) inner *= counts[b];
+    for (int b = 0; b < a; ++b) outer *= counts[b];
+    cudaError_t e = launch_line_c2c<double>(d_out, (int)n, inner, outer, sign > 0 ? +1 : -1, factorize(n), tw, s);
+    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: axis length exceeds the on-chip line limit");
+    GRFC_CUDA(e);
+  }
+  if (sign < 0) GRFC_CUDA(launch_scale_all<double>(d_out, P, 1.0 / (double)P, s));
+  return GRFC_OK;
+}
+
+}  // extern "C"

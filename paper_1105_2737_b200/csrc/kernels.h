@@ -1,0 +1,39 @@
+// Launcher declarations shared by the C-ABI (api.cu) and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "grfc_internal.cuh"
+
+namespace grfc {
+
+// Radix sequence of a line length (8s, then 4, 2, then odd primes).
+struct Factors {
+  int nf;
+  int r[40];
+};
+
+template <typename T>
+cudaError_t launch_gen_half(const GridDesc& g, const DensityDesc& D, int alg, double scale, uint64_t seed,
+                            uint64_t field0, const double2* injected, void* W, int64_t nfields, cudaStream_t s);
+template <typename T>
+cudaError_t launch_scale_half(const GridDesc& g, const DensityDesc& D, double scale, void* W, int64_t nfields,
+                              cudaStream_t s);
+template <typename T>
+cudaError_t launch_line_c2c(void* data, int n, int64_t inner, int64_t outer, int sign, const Factors& F,
+                            const void* tw, cudaStream_t s);
+template <typename T>
+cudaError_t launch_c2r_last(const void* W, void* out, int n, int64_t rows, int64_t rows_per_field,
+                            int64_t out_field_stride, int conj, const Factors& FM, const void* twN, cudaStream_t s);
+template <typename T>
+cudaError_t launch_r2c_last_noise(void* W, int n, int64_t rows, int64_t rows_per_field, uint64_t seed,
+                                  uint64_t field0, const double* injected, const Factors& FM, const void* twN,
+                                  cudaStream_t s);
+template <typename T>
+cudaError_t launch_scale_all(void* data, int64_t n, double sc, cudaStream_t s);
+template <typename T>
+cudaError_t launch_philox_pairs(const uint64_t* counters, int64_t n, uint64_t seed, uint64_t field, double* out,
+                                cudaStream_t s);
+
+}  // namespace grfc
