@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -187,7 +188,7 @@ static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64
   const int nd = (int)p->n[d - 1];
   const int64_t rows_pf = (int64_t)(p->points / (uint64_t)nd);
   const int64_t rows = rows_pf * nf;
-  if (p->fast && !inj_half && !inj_points) {
+  if (p->fast && !inj_half && !inj_points && stride % 2 == 0) {
     GRFC_CUDA(launch_fast2d(p->fast2d, p->alg, seed, field0, nf, W, out, stride, s));
     return GRFC_OK;
   }
@@ -390,7 +391,10 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
   }
   if (density->family == GRFC_DENSITY_TABLE) GRFC_CUDA(cudaMalloc(&p->d_table, p->cells * sizeof(double)));
   // Fused fast path for power-of-two 2D shapes (pow2_2d.cu).
-  if (density->family != GRFC_DENSITY_TABLE && fast2d_supported(dim, counts, dtype, algorithm, density->family)) {
+  // GRFC_DISABLE_FAST=1 forces the generic kernels (A/B parity testing).
+  const char* nofast = std::getenv("GRFC_DISABLE_FAST");
+  const bool allow_fast = !(nofast && nofast[0] == '1');
+  if (allow_fast && fast2d_supported(dim, counts, dtype, algorithm, density->family)) {
     GRFC_CUDA(fast2d_init(p->fast2d, p->g, p->D, dtype, algorithm, p->s_one, p->s_two));
     p->fast = true;
     p->path = fast2d_name(p->fast2d);
@@ -408,6 +412,7 @@ grfc_status grfc_plan_set_sqrt_gamma_table(grfc_plan p, const double* sg) {
   DeviceGuard guard(p->device);
   GRFC_CUDA(cudaMemcpy(p->d_table, sg, p->cells * sizeof(double), cudaMemcpyHostToDevice));
   p->D.table = p->d_table;
+  if (p->fast) p->fast2d.D.table = p->d_table;
   p->table_set = true;
   return GRFC_OK;
 }

@@ -1,0 +1,14 @@
+// Explicit instantiation of the fused pow2 2D kernels for one (dtype, column
+// length N1) pair; the Makefile compiles this file once per pair with
+// -DINST_T=<float|double> -DINST_N=<N1> so the objects build in parallel.
+// Rows are instantiated for M = N1/2 (covers every supported N2 = 2M).
+#include "fast2d_kernels.cuh"
+
+namespace grfc {
+template cudaError_t launch_cols<INST_T, INST_N, GRFC_ONE_FFT_OVERWRITE>(const Fast2D&, uint64_t, uint64_t, int64_t,
+                                                                        void*, cudaStream_t);
+template cudaError_t launch_cols<INST_T, INST_N, GRFC_ONE_FFT_RECURSIVE>(const Fast2D&, uint64_t, uint64_t, int64_t,
+                                                                        void*, cudaStream_t);
+template cudaError_t launch_rows<INST_T, INST_N / 2>(const Fast2D&, int64_t, const void*, void*, int64_t,
+                                                    cudaStream_t);
+}  // namespace grfc
