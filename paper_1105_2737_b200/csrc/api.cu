@@ -395,7 +395,9 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
   const char* nofast = std::getenv("GRFC_DISABLE_FAST");
   const bool allow_fast = !(nofast && nofast[0] == '1');
   if (allow_fast && fast2d_supported(dim, counts, dtype, algorithm, density->family)) {
-    GRFC_CUDA(fast2d_init(p->fast2d, p->g, p->D, dtype, algorithm, p->s_one, p->s_two));
+    cudaError_t e = fast2d_init(p->fast2d, p->g, p->D, dtype, algorithm, p->s_one, p->s_two);
+    if (e != cudaSuccess)
+      return fail(GRFC_ECUDA, std::string("CUDA: fast2d_init (") + p->fast2d.fail_what + "): " + cudaGetErrorString(e));
     p->fast = true;
     p->path = fast2d_name(p->fast2d);
   }
@@ -444,6 +446,13 @@ grfc_status grfc_generate(grfc_plan p, uint64_t seed, uint64_t first_field, uint
   if (nfields == 0) return GRFC_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  // Fused pow2 2D path: whole batch, pipelined internally (pow2_2d.cu).
+  if (p->fast && field_stride % 2 == 0) {
+    cudaError_t e = fast2d_generate(p->fast2d, p->alg, seed, first_field, (int64_t)nfields, d_out,
+                                    (int64_t)field_stride, s);
+    if (e != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: fused2d: ") + cudaGetErrorString(e));
+    return GRFC_OK;
+  }
   const int64_t chunk = chunk_fields(p, nfields);
   void* W = nullptr;
   GRFC_CUDA(cudaMallocAsync(&W, (size_t)chunk * p->cells * p->csize, s));
@@ -559,8 +568,12 @@ grfc_status grfc_dump_noise(grfc_plan p, uint64_t seed, uint64_t field, double* 
   GRFC_CUDA(cudaMalloc(&dctr, ctr.size() * sizeof(uint64_t)));
   GRFC_CUDA(cudaMalloc(&dpairs, ctr.size() * 2 * sizeof(double)));
   GRFC_CUDA(cudaMemcpy(dctr, ctr.data(), ctr.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  cudaError_t e = p->dtype == GRFC_F64 ? launch_philox_pairs<double>(dctr, (int64_t)ctr.size(), seed, field, dpairs, 0)
-                                       : launch_philox_pairs<float>(dctr, (int64_t)ctr.size(), seed, field, dpairs, 0);
+  // Unit count per algorithm: Alg 1 point pairs, Alg 2 H cells, Alg 3 lattice points.
+  const uint64_t U = p->alg == GRFC_TWO_FFT ? p->points / 2 : p->alg == GRFC_ONE_FFT_OVERWRITE ? p->cells : p->points;
+  const uint64_t Uh = (U + 1) / 2;
+  cudaError_t e = p->dtype == GRFC_F64
+                      ? launch_philox_pairs<double>(dctr, (int64_t)ctr.size(), Uh, seed, field, dpairs, 0)
+                      : launch_philox_pairs<float>(dctr, (int64_t)ctr.size(), Uh, seed, field, dpairs, 0);
   std::vector<double> pairs(ctr.size() * 2);
   if (e == cudaSuccess) e = cudaMemcpy(pairs.data(), dpairs, pairs.size() * sizeof(double), cudaMemcpyDeviceToHost);
   cudaFree(dctr);

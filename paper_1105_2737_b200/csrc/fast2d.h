@@ -20,7 +20,36 @@ struct Fast2D {
   double l2_budget = 48.0 * 1024 * 1024;  // bytes of workspace per chunk
   void* d_tw = nullptr;                   // twiddles
   int kind = 0;
+  // persistent fused kernel geometry (fused_query)
+  bool persistent = false;
+  int occ = 1, sms = 148, strips = 0, rtiles = 0;
+  // two-stream pipeline: column kernels on sa, row kernels on sb, a ring of
+  // kRing chunk slots ordered by events (no in-kernel waiting).
+  static constexpr int kRing = 3;
+  cudaStream_t sa = nullptr, sb = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_ja = nullptr, ev_jb = nullptr;
+  cudaEvent_t ev_cols[kRing] = {}, ev_rows[kRing] = {};
+  void* mu = nullptr;  // std::mutex*, serialises enqueue on the shared streams
+  int64_t chunk = 16;  // fields per pipeline chunk
+  const char* fail_what = "";
 };
+
+// Lookahead L (fields of column work ahead of row work) and ring slots S for
+// a batch of nf fields; conc = resident CTAs.
+inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S, uint32_t* conc) {
+  const uint32_t c = (uint32_t)(f.sms * f.occ), G = (uint32_t)(f.strips + f.rtiles);
+  uint32_t l = (4 * c + G - 1) / G;
+  l = l < 1 ? 1 : l;
+  l = l < (uint32_t)nf ? l : (uint32_t)nf;
+  uint32_t s = l + 2 * ((c + G - 1) / G) + 2;
+  s = s < (uint32_t)nf ? s : (uint32_t)nf;
+  *L = l;
+  *S = s;
+  *conc = c;
+}
+inline size_t fused_ctr_bytes(uint32_t S) { return ((1 + 2 * (size_t)S) * 4 + 255) / 256 * 256; }
+// Device workspace one persistent launch over nf fields needs.
+size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf);
 
 bool fast2d_supported(int d, const int64_t* n, int dtype, int alg, int family);
 cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int dtype, int alg, double s_one,
@@ -30,5 +59,8 @@ const char* fast2d_name(const Fast2D& f);
 // W: workspace of nf * |H| complex; out + i*stride (elements) = field i.
 cudaError_t launch_fast2d(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                           int64_t stride, cudaStream_t s);
+// Whole-batch generation on `s` (workspace, pipelining and ordering inside).
+cudaError_t fast2d_generate(Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* out,
+                            int64_t stride, cudaStream_t s);
 
 }  // namespace grfc

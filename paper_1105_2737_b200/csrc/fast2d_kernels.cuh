@@ -70,7 +70,18 @@ struct RowPlan {
     using R = Radices<__VA_ARGS__>;        \
   };
 GRFC_PLAN(ColPlan, 256, float, 16, 8, 16, 16)
+#ifndef GRFC_COL512
+#define GRFC_COL512 2
+#endif
+#if GRFC_COL512 == 1
+GRFC_PLAN(ColPlan, 512, float, 8, 4, 8, 8, 8)
+#elif GRFC_COL512 == 2
+GRFC_PLAN(ColPlan, 512, float, 16, 4, 16, 16, 2)
+#elif GRFC_COL512 == 3
+GRFC_PLAN(ColPlan, 512, float, 16, 8, 16, 16, 2)
+#else
 GRFC_PLAN(ColPlan, 512, float, 32, 8, 32, 16)
+#endif
 GRFC_PLAN(ColPlan, 1024, float, 32, 8, 32, 32)
 GRFC_PLAN(ColPlan, 2048, float, 16, 4, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, float, 16, 2, 16, 16, 16)
@@ -180,10 +191,13 @@ struct ColEx {
 template <typename C>
 struct RowEx {
   C* s;
+  bool active = true;  // idle teams (beyond the tile's rows) keep to the barriers only
   static constexpr int PER = 128 / (int)sizeof(C);
   __device__ __forceinline__ static int pad(int e) { return e + e / PER; }
-  __device__ __forceinline__ void put(int e, C v) { s[pad(e)] = v; }
-  __device__ __forceinline__ C get(int e) const { return s[pad(e)]; }
+  __device__ __forceinline__ void put(int e, C v) {
+    if (active) s[pad(e)] = v;
+  }
+  __device__ __forceinline__ C get(int e) const { return active ? s[pad(e)] : C{}; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 
@@ -197,24 +211,35 @@ struct F2Params {
   int n1, n2, m, hd;  // hd = N2/2 + 1
   double wstep1, wstep2;  // 2 pi / l
   double sqrt_c, alpha, ell, scale;
+  uint64_t uh;  // ceil(U/2): noise units per half Philox (grfc_internal.cuh unit_pair)
+  // fp32 copies for the SFU density path
+  float f_wstep1, f_wstep2, f_sqrt_c, f_ell2, f_nhalf_alpha, f_gauss_k, f_scale;
   int family;
   DensityDesc D;
   GridDesc g;
 };
 
-// sqrt(g) at the cell (k1, k2) of the half-lattice.
+// sqrt(g) at the cell (k1, k2) of the half-lattice. fp32 Matern/Gaussian use
+// float parameters and the SFU (ex2/lg2); everything else the generic
+// device evaluation (double inside).
 template <typename T>
 __device__ __forceinline__ T sqrt_g2(const F2Params& p, int k1, int k2) {
   const int k1w = k1 <= p.n1 / 2 ? k1 : k1 - p.n1;
   const int k2w = k2 <= p.n2 / 2 ? k2 : k2 - p.n2;
-  if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
-    const T w1 = (T)k1w * (T)p.wstep1, w2 = (T)k2w * (T)p.wstep2;
-    const T s = w1 * w1 + w2 * w2;
-    const T ell = (T)p.ell;
-    if (p.family == GRFC_DENSITY_GAUSSIAN_COV) return (T)p.sqrt_c * exp((T)(-0.25) * ell * ell * s);
-    const T q = (T)1 + ell * ell * s;
-    if constexpr (sizeof(T) == 4) return (T)p.sqrt_c * exp2f((float)(-0.5 * p.alpha) * __log2f(q));
-    else return (T)p.sqrt_c * pow(q, -0.5 * p.alpha);
+  if constexpr (sizeof(T) == 4) {
+    if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
+      const float w1 = (float)k1w * p.f_wstep1, w2 = (float)k2w * p.f_wstep2;
+      const float s = w1 * w1 + w2 * w2;
+      if (p.family == GRFC_DENSITY_GAUSSIAN_COV) return p.f_sqrt_c * ex2_approx(p.f_gauss_k * s);
+      return p.f_sqrt_c * ex2_approx(p.f_nhalf_alpha * lg2_approx(1.0f + p.f_ell2 * s));
+    }
+  } else {
+    if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
+      const double w1 = (double)k1w * p.wstep1, w2 = (double)k2w * p.wstep2;
+      const double s = w1 * w1 + w2 * w2;
+      if (p.family == GRFC_DENSITY_GAUSSIAN_COV) return p.sqrt_c * exp(-0.25 * p.ell * p.ell * s);
+      return p.sqrt_c * pow(1.0 + p.ell * p.ell * s, -0.5 * p.alpha);
+    }
   }
   int64_t kw[2] = {k1w, k2w};
   return sqrt_gamma<T>(p.g, p.D, kw, (int64_t)k1 * p.hd + k2);
@@ -222,47 +247,33 @@ __device__ __forceinline__ T sqrt_g2(const F2Params& p, int k1, int k2) {
 
 // X(K) = conj(w(K)) sqrt(g) scale for a half-lattice cell with the Philox
 // stream: the overwrite (Alg 2) / exact-set (Alg 3) rules of
-// philox_cell_noise (generic.cu) specialised to 2D.
+// philox_cell_noise (generic.cu) specialised to 2D, one Philox call per cell.
 template <typename T, int ALG>
-__device__ __forceinline__ C_t<T> gen_cell(const F2Params& p, int k1, int k2, uint64_t seed, uint64_t field) {
+__device__ __forceinline__ C_t<T> gen_cell(const F2Params& p, int k1, int k2, const PhiloxKey& key, uint64_t field) {
   using C = C_t<T>;
   const T r = (T)0.70710678118654752440;
   const bool edge = (k2 == 0 || k2 == p.m);
   const bool self = edge && (k1 == 0 || k1 == p.n1 / 2);
-  T z0, z1, wx, wy;
+  uint32_t u;
+  bool conj = false;
   if constexpr (ALG == GRFC_ONE_FFT_OVERWRITE) {
-    const int64_t h = (int64_t)k1 * p.hd + k2;
-    if (self) {
-      normal_pair<T>(seed, field, (uint64_t)h, z0, z1);
-      wx = z0;
-      wy = (T)0;
-    } else if (edge && k1 < p.n1 / 2) {  // mirror -K visited later: its draws, conjugated
-      const int64_t hm = (int64_t)(p.n1 - k1) * p.hd + k2;
-      normal_pair<T>(seed, field, (uint64_t)hm, z0, z1);
-      wx = r * z0;
-      wy = -r * z1;
+    if (edge && !self && k1 < p.n1 / 2) {  // mirror -K visited later: its draws, conjugated
+      u = (uint32_t)(p.n1 - k1) * p.hd + k2;
+      conj = true;
     } else {
-      normal_pair<T>(seed, field, (uint64_t)h, z0, z1);
-      wx = r * z0;
-      wy = r * z1;
+      u = (uint32_t)k1 * p.hd + k2;
     }
   } else {
-    if (self) {
-      normal_pair<T>(seed, field, (uint64_t)k1 * p.n2 + k2, z0, z1);
-      wx = z0;
-      wy = (T)0;
-    } else {
-      const bool k1_free = !(k1 == 0 || k1 == p.n1 / 2);
-      const bool rep = k1_free ? (k1 < p.n1 / 2) : true;
-      const int64_t lin = rep ? (int64_t)k1 * p.n2 + k2
-                              : (int64_t)((p.n1 - k1) % p.n1) * p.n2 + ((p.n2 - k2) % p.n2);
-      normal_pair<T>(seed, field, (uint64_t)lin, z0, z1);
-      wx = r * z0;
-      wy = rep ? r * z1 : -r * z1;
-    }
+    const bool rep = self || !(k1 != 0 && k1 != p.n1 / 2) || k1 < p.n1 / 2;
+    u = rep ? (uint32_t)k1 * p.n2 + k2 : (uint32_t)((p.n1 - k1) % p.n1) * p.n2 + ((p.n2 - k2) % p.n2);
+    conj = !rep;
   }
+  T z0, z1;
+  unit_pair<T>(key, field, u, p.uh, z0, z1);
   const T mlt = sqrt_g2<T>(p, k1, k2) * (T)p.scale;
-  return mk<C>(wx * mlt, -wy * mlt);
+  if (self) return mk<C>(z0 * mlt, (T)0);
+  const T wy = conj ? -r * z1 : r * z1;
+  return mk<C>(r * z0 * mlt, -wy * mlt);
 }
 
 // Slot -> column. Left slots [0, CB): k = s CB + c (k = 0 is the packed
@@ -295,41 +306,59 @@ __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
   return mk<C>(s.x - t.y, s.y + t.x);
 }
 
-// ---------------------------------------------------------------- kernels
+// ---------------------------------------------------------------- tiles
+// Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
+// generation fused in front and the Z epilogue behind. Block = col_threads.
 template <typename T, int N1, int ALG>
-__global__ void __launch_bounds__(col_threads<N1, T>())
-    k_cols_gen(F2Params p, uint64_t seed, uint64_t field0, C_t<T>* __restrict__ W,
-               const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
+__device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
+                                         const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
+                                         unsigned char* smem_raw) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
   constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
-  const int strips = p.m / (2 * CB);
-  const int s = (int)(blockIdx.x % (unsigned)strips);
-  const uint64_t f = blockIdx.x / (unsigned)strips;
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);
 
+  // Generation into shared memory (rolled loop: one copy of the Philox/Box-
+  // Muller/density code in the I-cache). Thread j owns rows j + t*TT.
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
+    // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one Philox call
+    const T r = (T)0.70710678118654752440, sc = (T)p.scale;
+#pragma unroll 2
+    for (int t = 0; t < E / 2; ++t) {
+      const int k1 = j + t * TT;
+      float a0, b0, a1, b1;
+      unit_quad_f32(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col), a0, b0, a1, b1);
+      const T m0 = sqrt_g2<T>(p, k1, col) * sc * r, m1 = sqrt_g2<T>(p, k1 + N1 / 2, col) * sc * r;
+      sm[k1 * SLOTS + slot] = mk<C>((T)a0 * m0, -(T)b0 * m0);
+      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)a1 * m1, -(T)b1 * m1);
+    }
+  } else {
+#pragma unroll 1
+    for (int t = 0; t < E; ++t) {
+      const int k1 = j + t * TT;
+      C x = gen_cell<T, ALG>(p, k1, col, key, fld);
+      if (packed) {  // column 0 + i * column M
+        const C y = gen_cell<T, ALG>(p, k1, p.m, key, fld);
+        x = mk<C>(x.x - y.y, x.y + y.x);
+      }
+      sm[k1 * SLOTS + slot] = x;
+    }
+  }
+  __syncthreads();
   C v[E];
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
 #pragma unroll
-    for (int i = 0; i < R0; ++i) {
-      const int k1 = j + b * TT + i * (N1 / R0);
-      C x = gen_cell<T, ALG>(p, k1, col, seed, field0 + f);
-      if (packed) {  // column 0 + i * column M
-        const C y = gen_cell<T, ALG>(p, k1, p.m, seed, field0 + f);
-        x = mk<C>(x.x - y.y, x.y + y.x);
-      }
-      v[b * R0 + i] = x;
-    }
-  ColEx<C, SLOTS> ex{reinterpret_cast<C*>(smem_raw), slot};
+    for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[(j + b * TT + i * (N1 / R0)) * SLOTS + slot];
+  __syncthreads();
+  ColEx<C, SLOTS> ex{sm, slot};
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
 
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
-  C* Wf = W + f * (uint64_t)N1 * (uint64_t)p.m;
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -339,38 +368,175 @@ __global__ void __launch_bounds__(col_threads<N1, T>())
       P.x = __shfl_xor_sync(0xffffffffu, v[e].x, CB);
       P.y = __shfl_xor_sync(0xffffffffu, v[e].y, CB);
       const int row = j + b * TT + i * (N1 / RL);
-      Wf[(int64_t)row * p.m + col] = epilogue_z<T>(v[e], P, packed, mid, w);
+      __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], P, packed, mid, w));
     }
+}
+
+// Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
+// real field rows out. Block = RPT * (M/E) threads.
+template <typename T, int M, int RPT>
+__device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
+                                         const C_t<T>* __restrict__ tw2, unsigned char* smem_raw) {
+  using C = C_t<T>;
+  using PL = RowPlan<M, T>;
+  constexpr int E = PL::E, TT = M / E;
+  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  const int tid = threadIdx.x, rl = tid / TT, j = tid % TT;
+  int row = r0 + rl;
+  const bool live = rl < RPT && row < nrows;
+  if (!live) row = nrows - 1;
+  const C* Wr = Wf + (int64_t)row * M;
+  C v[E];
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcg(&Wr[j + b * TT + i * (M / R0)]);
+  RowEx<C> ex{reinterpret_cast<C*>(smem_raw) + (rl < RPT ? rl : 0) * row_pitch<M, C>(), rl < RPT};
+  line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
+  if (!live) return;
+  C* o = reinterpret_cast<C*>(of + (int64_t)row * (2 * M));
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+    for (int i = 0; i < RL; ++i) __stcs(&o[j + b * TT + i * (M / RL)], v[b * RL + i]);
+}
+
+template <int N1, int M, typename T>
+constexpr int fused_threads() {
+  return col_threads<N1, T>();
+}
+// Rows per row tile: one team of M/E threads per row, capped so the row
+// exchange buffers fit 200 KB of shared memory (surplus teams idle).
+template <int N1, int M, typename T>
+constexpr int rows_per_tile() {
+  constexpr int teams = fused_threads<N1, M, T>() / (M / RowPlan<M, T>::E);
+  constexpr int cap = (int)(200 * 1024 / (row_pitch<M, C_t<T>>() * sizeof(C_t<T>)));
+  return teams < cap ? teams : cap;
+}
+template <int N1, int M, typename T>
+constexpr size_t fused_smem() {
+  using C = C_t<T>;
+  constexpr size_t a = (size_t)N1 * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
+  return a > b ? a : b;
+}
+
+// ---------------------------------------------------------------- persistent fused kernel
+// One launch per batch. Tiles are claimed in ticket order from
+//   C(0..L-1) | C(L) R(0) | C(L+1) R(1) | ... | R(F-L..F-1)
+// (C(f) = the column tiles of field f, R(f) = its row tiles), so column work
+// runs L fields ahead of row work. Field f's half-spectrum lives in ring slot
+// f mod S (S slots of P*s bytes: L2-resident). Per-slot counters order the
+// hand-offs: R(f) waits for C(f)'s tiles, C(f) waits until the rows of the
+// slot's previous field (f - S) are consumed. Every wait targets a smaller
+// ticket already held by a running CTA, so the queue cannot deadlock.
+struct F2Sched {
+  uint32_t* ticket;
+  uint32_t* col_done;  // [S]
+  uint32_t* row_done;  // [S]
+  uint32_t F, L, S, strips, rtiles;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Thread 0 polls with relaxed loads (no L1 invalidation per poll), then one
+// acquire load orders the consumer's reads after the producers' releases.
+__device__ __forceinline__ void wait_geq(const uint32_t* ctr, uint32_t target) {
+  if (threadIdx.x == 0) {
+    if (ld_relaxed_u32(ctr) < target)
+      while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
+    (void)ld_acquire_u32(ctr);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void signal_done(uint32_t* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+
+template <typename T, int N1, int M, int ALG>
+__global__ void __launch_bounds__(fused_threads<N1, M, T>())
+    k_fused2d(F2Params p, F2Sched q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring, T* __restrict__ out,
+              int64_t out_stride, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_ticket;
+  constexpr int RPT = rows_per_tile<N1, M, T>();
+  const uint64_t slot_elems = (uint64_t)N1 * M;
+  const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
+  const uint32_t total = q.F * G;
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(q.ticket, 1u);
+    __syncthreads();
+    uint32_t t = s_ticket;
+    if (t >= total) break;
+    bool col;
+    uint32_t f, idx;
+    if (t < pro) {
+      col = true;
+      f = t / q.strips;
+      idx = t % q.strips;
+    } else if ((t -= pro) < nfull * G) {
+      const uint32_t g = t / G, r = t % G;
+      col = r < q.strips;
+      f = col ? g + q.L : g;
+      idx = col ? r : r - q.strips;
+    } else {
+      t -= nfull * G;
+      col = false;
+      f = nfull + t / q.rtiles;
+      idx = t % q.rtiles;
+    }
+    const uint32_t slot = f % q.S, use = f / q.S;
+    C_t<T>* Wf = ring + slot * slot_elems;
+    if (col) {
+      wait_geq(&q.row_done[slot], use * q.rtiles);
+      col_tile<T, N1, ALG>(p, key, field0 + f, (int)idx, Wf, tw1, tw2, smem_raw);
+      signal_done(&q.col_done[slot]);
+    } else {
+      wait_geq(&q.col_done[slot], (use + 1) * q.strips);
+      row_tile<T, M, RPT>(Wf, (int)idx * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw);
+      signal_done(&q.row_done[slot]);
+    }
+  }
+}
+
+// Two-kernel variant (A/B and fallback): all column tiles of a chunk, then
+// all its row tiles.
+template <typename T, int N1, int ALG>
+__global__ void __launch_bounds__(col_threads<N1, T>())
+    k_cols_gen(F2Params p, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ W,
+               const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int strips = p.m / (2 * ColPlan<N1, T>::X);
+  const int s = (int)(blockIdx.x % (unsigned)strips);
+  const uint64_t f = blockIdx.x / (unsigned)strips;
+  col_tile<T, N1, ALG>(p, key, field0 + f, s, W + f * (uint64_t)N1 * (uint64_t)p.m, tw1, tw2, smem_raw);
 }
 
 template <typename T, int M>
 __global__ void __launch_bounds__(row_threads<M, T>())
     k_rows_c2r(const C_t<T>* __restrict__ W, T* __restrict__ out, int64_t rows, int rows_per_field,
                int64_t out_stride, const C_t<T>* __restrict__ tw2) {
-  using C = C_t<T>;
-  using PL = RowPlan<M, T>;
-  constexpr int E = PL::E, RPB = PL::X, TT = M / E;
-  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, rl = tid / TT, j = tid % TT;
-  int64_t row = (int64_t)blockIdx.x * RPB + rl;
-  const bool live = row < rows;
-  if (!live) row = rows - 1;
-  const C* Wr = W + row * M;
-  C v[E];
-#pragma unroll
-  for (int b = 0; b < E / R0; ++b)
-#pragma unroll
-    for (int i = 0; i < R0; ++i) v[b * R0 + i] = Wr[j + b * TT + i * (M / R0)];
-  RowEx<C> ex{reinterpret_cast<C*>(smem_raw) + rl * row_pitch<M, C>()};
-  line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
-  if (!live) return;
-  const int64_t f = row / rows_per_field, rr = row - f * rows_per_field;
-  C* o = reinterpret_cast<C*>(out + f * out_stride + rr * (int64_t)(2 * M));
-#pragma unroll
-  for (int b = 0; b < E / RL; ++b)
-#pragma unroll
-    for (int i = 0; i < RL; ++i) o[j + b * TT + i * (M / RL)] = v[b * RL + i];
+  constexpr int RPB = RowPlan<M, T>::X;
+  const int64_t r0 = (int64_t)blockIdx.x * RPB;
+  const int64_t f = r0 / rows_per_field;
+  row_tile<T, M, RPB>(W + f * (int64_t)rows_per_field * M, (int)(r0 - f * rows_per_field), rows_per_field,
+                      out + f * out_stride, tw2, smem_raw);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -387,6 +553,14 @@ inline F2Params make_params(const Fast2D& f) {
   p.alpha = f.D.alpha;
   p.ell = f.D.family == GRFC_DENSITY_MATERN ? f.D.r[1] : f.D.r[0];
   p.scale = f.s_one;
+  p.uh = f.alg == GRFC_ONE_FFT_OVERWRITE ? ((uint64_t)f.n1 * (f.n2 / 2 + 1) + 1) / 2 : ((uint64_t)f.n1 * f.n2 + 1) / 2;
+  p.f_wstep1 = (float)p.wstep1;
+  p.f_wstep2 = (float)p.wstep2;
+  p.f_sqrt_c = (float)p.sqrt_c;
+  p.f_ell2 = (float)(p.ell * p.ell);
+  p.f_nhalf_alpha = (float)(-0.5 * p.alpha);
+  p.f_gauss_k = (float)(-0.25 * p.ell * p.ell * 1.4426950408889634);  // -ell^2/4 * log2(e)
+  p.f_scale = (float)p.scale;
   p.D = f.D;
   p.g = f.g;
   return p;
@@ -407,7 +581,7 @@ cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t
   const C* tw1 = (const C*)f.d_tw;
   const C* tw2 = tw1 + f.n1;
   LaunchScope ls("fused_cols_gen", s);
-  k_cols_gen<T, N1, ALG><<<(unsigned)(nf * strips), col_threads<N1, T>(), smem, s>>>(make_params(f), seed, field0,
+  k_cols_gen<T, N1, ALG><<<(unsigned)(nf * strips), col_threads<N1, T>(), smem, s>>>(make_params(f), philox_key(seed), field0,
                                                                                      (C*)W, tw1, tw2);
   return cudaGetLastError();
 }
@@ -428,6 +602,53 @@ cudaError_t launch_rows(const Fast2D& f, int64_t nf, const void* W, void* out, i
   LaunchScope ls("fused_rows_c2r", s);
   k_rows_c2r<T, M><<<(unsigned)((rows + RPB - 1) / RPB), row_threads<M, T>(), smem, s>>>(
       (const C*)W, (T*)out, rows, f.n1, stride, tw2);
+  return cudaGetLastError();
+}
+
+// Fills the persistent-kernel geometry of Fast2D (called once at plan setup).
+template <typename T, int N1, int M, int ALG>
+cudaError_t fused_query(Fast2D& f) {
+  constexpr int NT = fused_threads<N1, M, T>(), RPT = rows_per_tile<N1, M, T>();
+  constexpr size_t smem = fused_smem<N1, M, T>();
+  cudaError_t e = cudaFuncSetAttribute(k_fused2d<T, N1, M, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0, dev = 0, sms = 148;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<T, N1, M, ALG>, NT, smem);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  f.occ = occ < 1 ? 1 : occ;
+  f.sms = sms;
+  f.strips = M / (2 * ColPlan<N1, T>::X);
+  f.rtiles = N1 / RPT;
+  return cudaSuccess;
+}
+
+template <typename T, int N1, int M, int ALG>
+cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
+                         int64_t stride, cudaStream_t s) {
+  using C = C_t<T>;
+  constexpr int NT = fused_threads<N1, M, T>();
+  constexpr size_t smem = fused_smem<N1, M, T>();
+  F2Sched q{};
+  uint32_t conc = 0;
+  fused_geometry(f, nf, &q.L, &q.S, &conc);
+  q.F = (uint32_t)nf;
+  q.strips = (uint32_t)f.strips;
+  q.rtiles = (uint32_t)f.rtiles;
+  uint32_t* ctr = (uint32_t*)ws;  // [ticket][col_done S][row_done S] | ring
+  q.ticket = ctr;
+  q.col_done = ctr + 1;
+  q.row_done = ctr + 1 + q.S;
+  C* ring = (C*)((char*)ws + fused_ctr_bytes(q.S));
+  cudaError_t e = cudaMemsetAsync(ctr, 0, (1 + 2 * q.S) * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const C* tw1 = (const C*)f.d_tw;
+  const C* tw2 = tw1 + f.n1;
+  const uint32_t total = q.F * (q.strips + q.rtiles);
+  const uint32_t grid = total < conc ? total : conc;
+  LaunchScope ls("fused2d_persistent", s);
+  k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(make_params(f), q, philox_key(seed), field0, ring, (T*)out, stride, tw1, tw2);
   return cudaGetLastError();
 }
 

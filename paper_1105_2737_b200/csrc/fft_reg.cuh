@@ -83,12 +83,13 @@ __device__ __forceinline__ C twmul(C v) {
     constexpr R h = (R)0.70710678118654752440;
     constexpr R c = (R)(cos_2pi(k, N) > 0 ? 1 : -1) * h;
     constexpr R s = (R)(SIGN * (sin_2pi(k, N) > 0 ? 1 : -1)) * h;
-    if constexpr (c == s) return mk<C>((v.x - v.y) * c, (v.x + v.y) * c);
-    else return mk<C>((v.x + v.y) * c, (v.y - v.x) * c);
+    // (c + i s) v with |c| = |s|: c * (v + i (s/c) v)
+    const C t = (c == s) ? mul_si<+1>(v) : mul_si<-1>(v);
+    return cscale(cadd(v, t), c);
   } else {
     constexpr R c = (R)cos_2pi(k, N);
     constexpr R s = (R)(SIGN * sin_2pi(k, N));
-    return mk<C>(v.x * c - v.y * s, v.x * s + v.y * c);
+    return cmul_cs(v, c, s);
   }
 }
 

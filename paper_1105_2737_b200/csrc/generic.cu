@@ -160,56 +160,51 @@ __device__ __forceinline__ void wrap_freq(const GridDesc& g, const int64_t* k, i
 //    (hermitian.cpp:39-84 membership); conjugated when K != rep(K).
 template <typename T>
 __device__ __forceinline__ C_t<T> philox_cell_noise(const GridDesc& g, int alg, const int64_t* k, int64_t h,
-                                                    uint64_t seed, uint64_t field) {
+                                                    const PhiloxKey& key, uint64_t field) {
   using C = C_t<T>;
   const T r = (T)0.70710678118654752440;
   bool self = true;
   for (int a = 0; a < g.d; ++a)
     if (k[a] != 0 && k[a] != g.n[a] / 2) self = false;
-  T z0, z1;
+  uint64_t u, Uh;
+  bool conj = false;
   if (alg == GRFC_ONE_FFT_OVERWRITE) {
-    if (self) {
-      normal_pair<T>(seed, field, (uint64_t)h, z0, z1);
-      return mk<C>(z0, (T)0);
-    }
+    Uh = ((uint64_t)g.cells + 1) / 2;
+    u = (uint64_t)h;
     const int64_t kd = k[g.d - 1];
-    if (kd == 0 || kd == g.n[g.d - 1] / 2) {
+    if (!self && (kd == 0 || kd == g.n[g.d - 1] / 2)) {
       int64_t hm = 0;
       for (int a = 0; a < g.d - 1; ++a) hm = hm * g.n[a] + (k[a] == 0 ? 0 : g.n[a] - k[a]);
       hm = hm * g.hd + kd;
       if (hm > h) {
-        normal_pair<T>(seed, field, (uint64_t)hm, z0, z1);
-        return mk<C>(r * z0, -r * z1);
+        u = (uint64_t)hm;
+        conj = true;
       }
     }
-    normal_pair<T>(seed, field, (uint64_t)h, z0, z1);
-    return mk<C>(r * z0, r * z1);
+  } else {  // exact set
+    Uh = ((uint64_t)g.points + 1) / 2;
+    bool is_rep = true;
+    if (!self)
+      for (int a = 0; a < g.d; ++a)
+        if (k[a] != 0 && k[a] != g.n[a] / 2) {
+          is_rep = k[a] < g.n[a] / 2;
+          break;
+        }
+    int64_t lin = 0;
+    for (int a = 0; a < g.d; ++a) lin = lin * g.n[a] + (is_rep ? k[a] : (k[a] == 0 ? 0 : g.n[a] - k[a]));
+    u = (uint64_t)lin;
+    conj = !is_rep;
   }
-  // exact set
-  int64_t lin = 0;
-  if (self) {
-    for (int a = 0; a < g.d; ++a) lin = lin * g.n[a] + k[a];
-    normal_pair<T>(seed, field, (uint64_t)lin, z0, z1);
-    return mk<C>(z0, (T)0);
-  }
-  bool is_rep = true;
-  for (int a = 0; a < g.d; ++a)
-    if (k[a] != 0 && k[a] != g.n[a] / 2) {
-      is_rep = k[a] < g.n[a] / 2;
-      break;
-    }
-  for (int a = 0; a < g.d; ++a) {
-    const int64_t ka = is_rep ? k[a] : (k[a] == 0 ? 0 : g.n[a] - k[a]);
-    lin = lin * g.n[a] + ka;
-  }
-  normal_pair<T>(seed, field, (uint64_t)lin, z0, z1);
-  return is_rep ? mk<C>(r * z0, r * z1) : mk<C>(r * z0, -r * z1);
+  T z0, z1;
+  unit_pair<T>(key, field, u, Uh, z0, z1);
+  if (self) return mk<C>(z0, (T)0);
+  return mk<C>(r * z0, conj ? -r * z1 : r * z1);
 }
 
 // ---------------------------------------------------------------- kernels
 // X(K) = conj(w(K)) * sqrt(g) * scale on H, for nfields fields.
 template <typename T>
-__global__ void k_gen_half(GridDesc g, DensityDesc D, int alg, T scale, uint64_t seed, uint64_t field0,
+__global__ void k_gen_half(GridDesc g, DensityDesc D, int alg, T scale, PhiloxKey key, uint64_t field0,
                            const double2* injected, C_t<T>* W, int64_t nfields) {
   using C = C_t<T>;
   const int64_t total = g.cells * nfields;
@@ -224,7 +219,7 @@ __global__ void k_gen_half(GridDesc g, DensityDesc D, int alg, T scale, uint64_t
       const double2 v = injected[h];
       w = mk<C>((T)v.x, (T)v.y);
     } else {
-      w = philox_cell_noise<T>(g, alg, k, h, seed, field0 + (uint64_t)f);
+      w = philox_cell_noise<T>(g, alg, k, h, key, field0 + (uint64_t)f);
     }
     const T m = sqrt_gamma<T>(g, D, kw, h) * scale;
     W[t] = mk<C>(w.x * m, -w.y * m);
@@ -335,7 +330,7 @@ __global__ void k_c2r_last(const C_t<T>* W, T* out, int n, int64_t rows, int64_t
 //   z[m] = x[2m] + i x[2m+1]; Z = DFT+_M(z);
 //   X[k] = 1/2 (Z[k] + conj(Z[M-k])) - i/2 e^{+2 pi i k/n} (Z[k] - conj(Z[M-k]))
 template <typename T>
-__global__ void k_r2c_last_noise(C_t<T>* W, int n, int64_t rows, int64_t rows_per_field, uint64_t seed,
+__global__ void k_r2c_last_noise(C_t<T>* W, int n, int64_t rows, int64_t rows_per_field, PhiloxKey key,
                                  uint64_t field0, const double* injected, int RB, Factors F,
                                  const C_t<T>* twN) {
   using C = C_t<T>;
@@ -354,7 +349,7 @@ __global__ void k_r2c_last_noise(C_t<T>* W, int n, int64_t rows, int64_t rows_pe
       z0 = (T)injected[2 * pair];
       z1 = (T)injected[2 * pair + 1];
     } else {
-      normal_pair<T>(seed, field0 + (uint64_t)f, (uint64_t)pair, z0, z1);
+      unit_pair<T>(key, field0 + (uint64_t)f, (uint64_t)pair, (uint64_t)(rows_per_field * M + 1) / 2, z0, z1);
     }
     a[l * pitch + m] = mk<C>(z0, z1);
   }
@@ -380,10 +375,11 @@ __global__ void k_scale_all(C_t<T>* data, int64_t n, T s) {
 
 // Philox noise for a list of counters (the dump path): out[2i], out[2i+1].
 template <typename T>
-__global__ void k_philox_pairs(const uint64_t* counters, int64_t n, uint64_t seed, uint64_t field, double* out) {
+__global__ void k_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, PhiloxKey key, uint64_t field,
+                               double* out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     T z0, z1;
-    normal_pair<T>(seed, field, counters[t], z0, z1);
+    unit_pair<T>(key, field, units[t], Uh, z0, z1);
     out[2 * t] = (double)z0;
     out[2 * t + 1] = (double)z1;
   }
@@ -399,7 +395,7 @@ template <typename T>
 cudaError_t launch_gen_half(const GridDesc& g, const DensityDesc& D, int alg, double scale, uint64_t seed,
                             uint64_t field0, const double2* injected, void* W, int64_t nfields, cudaStream_t s) {
   LaunchScope ls_("gen_half", s);
-  k_gen_half<T><<<grid_for(g.cells * nfields, 256), 256, 0, s>>>(g, D, alg, (T)scale, seed, field0, injected,
+  k_gen_half<T><<<grid_for(g.cells * nfields, 256), 256, 0, s>>>(g, D, alg, (T)scale, philox_key(seed), field0, injected,
                                                                  (C_t<T>*)W, nfields);
   return cudaGetLastError();
 }
@@ -477,7 +473,7 @@ cudaError_t launch_r2c_last_noise(void* W, int n, int64_t rows, int64_t rows_per
   const size_t smem = RB * per_row;
   const int64_t blocks = (rows + RB - 1) / RB;
   cudaFuncSetAttribute(k_r2c_last_noise<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_r2c_last_noise<T><<<(unsigned)blocks, 256, smem, s>>>((C*)W, n, rows, rows_per_field, seed, field0, injected,
+  k_r2c_last_noise<T><<<(unsigned)blocks, 256, smem, s>>>((C*)W, n, rows, rows_per_field, philox_key(seed), field0, injected,
                                                          RB, FM, (const C*)twN);
   return cudaGetLastError();
 }
@@ -490,10 +486,10 @@ cudaError_t launch_scale_all(void* data, int64_t n, double sc, cudaStream_t s) {
 }
 
 template <typename T>
-cudaError_t launch_philox_pairs(const uint64_t* counters, int64_t n, uint64_t seed, uint64_t field, double* out,
-                                cudaStream_t s) {
+cudaError_t launch_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, uint64_t seed, uint64_t field,
+                                double* out, cudaStream_t s) {
   LaunchScope ls_("philox_pairs", s);
-  k_philox_pairs<T><<<grid_for(n, 256), 256, 0, s>>>(counters, n, seed, field, out);
+  k_philox_pairs<T><<<grid_for(n, 256), 256, 0, s>>>(units, n, Uh, philox_key(seed), field, out);
   return cudaGetLastError();
 }
 
@@ -509,7 +505,8 @@ cudaError_t launch_philox_pairs(const uint64_t* counters, int64_t n, uint64_t se
   template cudaError_t launch_r2c_last_noise<T>(void*, int, int64_t, int64_t, uint64_t, uint64_t, const double*, \
                                                 const Factors&, const void*, cudaStream_t);                     \
   template cudaError_t launch_scale_all<T>(void*, int64_t, double, cudaStream_t);                               \
-  template cudaError_t launch_philox_pairs<T>(const uint64_t*, int64_t, uint64_t, uint64_t, double*, cudaStream_t);
+  template cudaError_t launch_philox_pairs<T>(const uint64_t*, int64_t, uint64_t, uint64_t, uint64_t, double*, \
+                                                   cudaStream_t);
 
 GRFC_INSTANTIATE(float)
 GRFC_INSTANTIATE(double)

@@ -56,32 +56,95 @@ __device__ __forceinline__ C mul_si(C a) {
   return SIGN > 0 ? mk<C>(-a.y, a.x) : mk<C>(a.y, -a.x);
 }
 
+// ---- float2 specialisations on the sm_100 packed fp32x2 pipe (FADD2 / FMUL2 /
+// FFMA2). ptxas folds the broadcast (.F32), swap (.LO_HI) and partial-negate
+// operand forms, so a complex add is 1 instruction and a complex multiply 2.
+__device__ __forceinline__ unsigned long long f2pk(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2upk(unsigned long long r) {
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2upk(f2add(f2pk(a.x, a.y), f2pk(b.x, b.y))); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return f2upk(f2sub(f2pk(a.x, a.y), f2pk(b.x, b.y))); }
+// a * w = w.x (a.x, a.y) + w.y (-a.y, a.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+  const unsigned long long t = f2mul(f2pk(w.x, w.x), f2pk(a.x, a.y));
+  return f2upk(f2fma(f2pk(w.y, w.y), f2pk(-a.y, a.x), t));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return f2upk(f2mul(f2pk(s, s), f2pk(a.x, a.y))); }
+// a * (c + i s) with c, s constants
+__device__ __forceinline__ float2 cmul_cs(float2 a, float c, float s) {
+  const unsigned long long t = f2mul(f2pk(c, c), f2pk(a.x, a.y));
+  return f2upk(f2fma(f2pk(s, s), f2pk(-a.y, a.x), t));
+}
+template <typename C>
+__device__ __forceinline__ C cmul_cs(C a, decltype(C{}.x) c, decltype(C{}.x) s) {
+  return mk<C>(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+
 // ---------------------------------------------------------------- Philox
 // Philox4x32-10 (Salmon et al., SC'11): counter (cell_lo, cell_hi, field_lo,
 // field_hi), key (seed_lo, seed_hi). Fixed key scheme, documented in
 // DESIGN.md §Noise; never change it (fields must stay re-generable).
-__host__ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+// Round keys precomputed on the host (k[2r], k[2r+1]) = (seed_lo + r W0,
+// seed_hi + r W1): a round is then 2 IMAD.WIDE.U32 + 2 LOP3 with the keys
+// read straight from the kernel-parameter constant bank.
+struct PhiloxKey {
+  uint32_t k[20];
+};
+
+inline PhiloxKey philox_key(uint64_t seed) {
+  PhiloxKey K;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    K.k[2 * r] = k0;
+    K.k[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return K;
+}
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKey& K) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-#ifdef __CUDA_ARCH__
-    const uint32_t hi0 = __umulhi(M0, c.x), hi1 = __umulhi(M1, c.z);
-#else
-    const uint32_t hi0 = (uint32_t)(((uint64_t)M0 * c.x) >> 32);
-    const uint32_t hi1 = (uint32_t)(((uint64_t)M1 * c.z) >> 32);
-#endif
-    const uint32_t lo0 = M0 * c.x, lo1 = M1 * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += W0;
-    k.y += W1;
+    const uint64_t p0 = (uint64_t)M0 * c.x, p1 = (uint64_t)M1 * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ K.k[2 * r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ K.k[2 * r + 1],
+                   (uint32_t)p0);
   }
   return c;
 }
 
-__host__ __device__ __forceinline__ uint4 philox_draw(uint64_t seed, uint64_t field, uint64_t cell) {
-  return philox4x32_10(make_uint4((uint32_t)cell, (uint32_t)(cell >> 32), (uint32_t)field,
-                                  (uint32_t)(field >> 32)),
-                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+__device__ __forceinline__ uint4 philox_draw(const PhiloxKey& K, uint64_t field, uint64_t cell) {
+  return philox4x32_10(make_uint4((uint32_t)cell, (uint32_t)(cell >> 32), (uint32_t)field, (uint32_t)(field >> 32)),
+                       K);
 }
 
 // Box-Muller pair. fp32: 24-bit uniforms from x, y; u1 in (0,1], angle
@@ -90,13 +153,35 @@ __host__ __device__ __forceinline__ uint4 philox_draw(uint64_t seed, uint64_t fi
 template <typename T>
 __device__ __forceinline__ void box_muller(uint4 r, T& z0, T& z1);
 
+// fp32 SFU forms (MUFU.LG2 / .SQRT / .SIN / .COS): the noise definition itself,
+// shared bit-for-bit by generation and grfc_dump_noise.
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void sincos_approx(float x, float& s, float& c) {
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(x));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(x));
+}
+
 template <>
 __device__ __forceinline__ void box_muller<float>(uint4 r, float& z0, float& z1) {
-  const float u1 = (float)((r.x >> 8) + 1u) * 0x1.0p-24f;
-  const float u2 = (float)(r.y >> 8) * 0x1.0p-24f;
-  const float rad = sqrtf(-2.0f * __logf(u1));
+  const float u1 = (float)((r.x >> 8) + 1u) * 0x1.0p-24f;  // (0, 1]
+  const float u2 = (float)(r.y >> 8) * 0x1.0p-24f;         // [0, 1)
+  const float rad = sqrt_approx(-1.38629436111989061883f * lg2_approx(u1));  // sqrt(-2 ln u1)
   float s, c;
-  __sincosf(6.2831853071795865f * (u2 - 0.5f), &s, &c);
+  sincos_approx(6.28318530717958647693f * u2 - 3.14159265358979323846f, s, c);
   z0 = rad * c;
   z1 = rad * s;
 }
@@ -115,8 +200,41 @@ __device__ __forceinline__ void box_muller<double>(uint4 r, double& z0, double& 
 }
 
 template <typename T>
-__device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t field, uint64_t cell, T& z0, T& z1) {
-  box_muller<T>(philox_draw(seed, field, cell), z0, z1);
+__device__ __forceinline__ void normal_pair(const PhiloxKey& K, uint64_t field, uint64_t cell, T& z0, T& z1) {
+  box_muller<T>(philox_draw(K, field, cell), z0, z1);
+}
+
+// Noise units. Every algorithm draws one N(0,1) pair (a_u, b_u) per "unit" u
+// of a field: Alg 2 the half-lattice cell index, Alg 3 the full-lattice index
+// of a representative, Alg 1 the point pair J/2. With
+// U units and Uh = ceil(U/2):
+//   fp64: Philox counter u, all 128 bits feed one pair (53-bit uniforms);
+//   fp32: Philox counter u mod Uh; words (x, y) feed unit u < Uh and
+//         words (z, w) feed unit u + Uh — one call serves two units.
+__device__ __forceinline__ void box_muller_f32(uint32_t x, uint32_t y, float& z0, float& z1) {
+  box_muller<float>(make_uint4(x, y, 0u, 0u), z0, z1);
+}
+
+template <typename T>
+__device__ __forceinline__ void unit_pair(const PhiloxKey& K, uint64_t field, uint64_t u, uint64_t Uh, T& z0, T& z1) {
+  if constexpr (sizeof(T) == 8) {
+    normal_pair<T>(K, field, u, z0, z1);
+  } else {
+    const bool hi = u >= Uh;
+    const uint4 r = philox_draw(K, field, hi ? u - Uh : u);
+    float a, b;
+    box_muller_f32(hi ? r.z : r.x, hi ? r.w : r.y, a, b);
+    z0 = a;
+    z1 = b;
+  }
+}
+
+// fp32: both units of one Philox call, u (< Uh) and u + Uh.
+__device__ __forceinline__ void unit_quad_f32(const PhiloxKey& K, uint64_t field, uint64_t u, float& a0, float& b0,
+                                              float& a1, float& b1) {
+  const uint4 r = philox_draw(K, field, u);
+  box_muller_f32(r.x, r.y, a0, b0);
+  box_muller_f32(r.z, r.w, a1, b1);
 }
 
 // ---------------------------------------------------------------- grid

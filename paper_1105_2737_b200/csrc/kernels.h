@@ -33,7 +33,7 @@ cudaError_t launch_r2c_last_noise(void* W, int n, int64_t rows, int64_t rows_per
 template <typename T>
 cudaError_t launch_scale_all(void* data, int64_t n, double sc, cudaStream_t s);
 template <typename T>
-cudaError_t launch_philox_pairs(const uint64_t* counters, int64_t n, uint64_t seed, uint64_t field, double* out,
-                                cudaStream_t s);
+cudaError_t launch_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, uint64_t seed, uint64_t field,
+                                double* out, cudaStream_t s);
 
 }  // namespace grfc

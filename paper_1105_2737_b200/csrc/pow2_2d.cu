@@ -2,6 +2,8 @@
 // live in fast2d_kernels.cuh and are instantiated per (dtype, size) by
 // fast2d_inst.cu (one object per combination, compiled in parallel).
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "fast2d.h"
@@ -14,6 +16,11 @@ template <typename T, int N1, int ALG>
 cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, cudaStream_t s);
 template <typename T, int M>
 cudaError_t launch_rows(const Fast2D& f, int64_t nf, const void* W, void* out, int64_t stride, cudaStream_t s);
+template <typename T, int N1, int M, int ALG>
+cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
+                         int64_t stride, cudaStream_t s);
+template <typename T, int N1, int M, int ALG>
+cudaError_t fused_query(Fast2D& f);
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 
@@ -65,9 +72,47 @@ static cudaError_t dispatch_rows(const Fast2D& f, int64_t nf, const void* W, voi
   return cudaErrorNotSupported;
 }
 
+// (N1, M) -> instantiation; F is a functor template taking <N1, M>.
+#define GRFC_DISPATCH_M(T, N1, ALG, CALL)                   \
+  switch (f.n2 / 2) {                                      \
+    case 128: return CALL(T, N1, 128, ALG);                \
+    case 256: return CALL(T, N1, 256, ALG);                \
+    case 512: return CALL(T, N1, 512, ALG);                \
+    case 1024: return CALL(T, N1, 1024, ALG);              \
+    case 2048: return CALL(T, N1, 2048, ALG);              \
+  }                                                        \
+  return cudaErrorNotSupported;
+#define GRFC_DISPATCH_N1(T, ALG, CALL)                      \
+  switch (f.n1) {                                          \
+    case 256: { GRFC_DISPATCH_M(T, 256, ALG, CALL) }       \
+    case 512: { GRFC_DISPATCH_M(T, 512, ALG, CALL) }       \
+    case 1024: { GRFC_DISPATCH_M(T, 1024, ALG, CALL) }     \
+    case 2048: { GRFC_DISPATCH_M(T, 2048, ALG, CALL) }     \
+    case 4096: { GRFC_DISPATCH_M(T, 4096, ALG, CALL) }     \
+  }                                                        \
+  return cudaErrorNotSupported;
+
+#define GRFC_CALL_FUSED(T, N1, M, ALG) launch_fused<T, N1, M, ALG>(f, seed, field0, nf, W, out, stride, s)
+#define GRFC_CALL_QUERY(T, N1, M, ALG) fused_query<T, N1, M, ALG>(f)
+
+template <typename T, int ALG>
+static cudaError_t dispatch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
+                                  int64_t stride, cudaStream_t s) {
+  GRFC_DISPATCH_N1(T, ALG, GRFC_CALL_FUSED)
+}
+
+template <typename T, int ALG>
+static cudaError_t dispatch_query(Fast2D& f) {
+  GRFC_DISPATCH_N1(T, ALG, GRFC_CALL_QUERY)
+}
+
 template <typename T>
 static cudaError_t run_fast(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                             int64_t stride, cudaStream_t s) {
+  if (f.persistent)
+    return alg == GRFC_ONE_FFT_OVERWRITE
+               ? dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s)
+               : dispatch_fused<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, out, stride, s);
   cudaError_t e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_cols<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, s)
                                                 : dispatch_cols<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, s);
   if (e != cudaSuccess) return e;
@@ -85,6 +130,7 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   f.s_one = s_one;
   f.s_two = s_two;
   const size_t cs = dtype == GRFC_F64 ? 16 : 8;
+  f.fail_what = "twiddle upload";
   cudaError_t e = cudaMalloc(&f.d_tw, (size_t)(f.n1 + f.n2) * cs);
   if (e != cudaSuccess) return e;
   if (dtype == GRFC_F64) {
@@ -96,14 +142,111 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
     a.insert(a.end(), b.begin(), b.end());
     e = cudaMemcpy(f.d_tw, a.data(), a.size() * cs, cudaMemcpyHostToDevice);
   }
-  // Keep the per-chunk workspace (P*s bytes per field) well inside the 126 MB L2.
+  if (e != cudaSuccess) return e;
+  // Pipeline chunk: ~12 MiB of half-spectrum per slot, 3 slots in flight (L2-resident).
+  const double slot = (double)f.n1 * (f.n2 / 2) * cs;
+  f.chunk = (int64_t)std::max(1.0, std::floor(12.0 * 1024 * 1024 / slot));
   f.l2_budget = 40.0 * 1024 * 1024;
+  f.fail_what = "pipeline streams";
+  e = cudaStreamCreateWithFlags(&f.sa, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&f.sb, cudaStreamNonBlocking);
+  cudaEvent_t* evs[] = {&f.ev_fork, &f.ev_ja, &f.ev_jb};
+  for (auto* ev : evs)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  for (int i = 0; i < Fast2D::kRing && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&f.ev_cols[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f.ev_rows[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return e;
+  f.mu = new std::mutex();
+  // Default: the single-launch persistent kernel; GRFC_PERSISTENT=0 selects the
+  // two-stream column/row kernel pipeline (A/B testing).
+  const char* pe = std::getenv("GRFC_PERSISTENT");
+  f.persistent = !(pe && pe[0] == '0');
+  if (!f.persistent) return cudaSuccess;
+  f.fail_what = "persistent kernel query";
+  if (dtype == GRFC_F64)
+    e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
+                                      : dispatch_query<double, GRFC_ONE_FFT_RECURSIVE>(f);
+  else
+    e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f)
+                                      : dispatch_query<float, GRFC_ONE_FFT_RECURSIVE>(f);
   return e;
+}
+
+size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf) {
+  const size_t slot = (size_t)f.n1 * (size_t)(f.n2 / 2) * (f.dtype == GRFC_F64 ? 16 : 8);
+  if (!f.persistent) return slot * (size_t)nf;
+  uint32_t L, S, c;
+  fused_geometry(f, nf, &L, &S, &c);
+  return fused_ctr_bytes(S) + slot * S;
 }
 
 void fast2d_free(Fast2D& f) {
   cudaFree(f.d_tw);
   f.d_tw = nullptr;
+  if (f.sa) cudaStreamDestroy(f.sa);
+  if (f.sb) cudaStreamDestroy(f.sb);
+  cudaEvent_t evs[] = {f.ev_fork, f.ev_ja, f.ev_jb};
+  for (auto ev : evs)
+    if (ev) cudaEventDestroy(ev);
+  for (int i = 0; i < Fast2D::kRing; ++i) {
+    if (f.ev_cols[i]) cudaEventDestroy(f.ev_cols[i]);
+    if (f.ev_rows[i]) cudaEventDestroy(f.ev_rows[i]);
+  }
+  delete static_cast<std::mutex*>(f.mu);
+  f.mu = nullptr;
+}
+
+template <typename T>
+static cudaError_t launch_cols_any(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W,
+                                   cudaStream_t s) {
+  return alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_cols<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, s)
+                                       : dispatch_cols<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, s);
+}
+
+cudaError_t fast2d_generate(Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* out,
+                            int64_t stride, cudaStream_t s) {
+  const size_t esz = f.dtype == GRFC_F64 ? 8 : 4;
+  void* ws = nullptr;
+  if (f.persistent) {
+    cudaError_t e = cudaMallocAsync(&ws, fast2d_workspace_bytes(f, nf), s);
+    if (e != cudaSuccess) return e;
+    e = launch_fast2d(f, alg, seed, field0, nf, ws, out, stride, s);
+    cudaFreeAsync(ws, s);
+    return e;
+  }
+  std::lock_guard<std::mutex> lock(*static_cast<std::mutex*>(f.mu));
+  const int64_t chunk = std::min<int64_t>(f.chunk, nf);
+  const size_t slot_bytes = (size_t)chunk * f.n1 * (f.n2 / 2) * 2 * esz;
+  const int ring = (int)std::min<int64_t>(Fast2D::kRing, (nf + chunk - 1) / chunk);
+  cudaError_t e = cudaMallocAsync(&ws, slot_bytes * ring, s);
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(f.ev_fork, s);
+  cudaStreamWaitEvent(f.sa, f.ev_fork, 0);
+  cudaStreamWaitEvent(f.sb, f.ev_fork, 0);
+  int i = 0;
+  for (int64_t f0 = 0; f0 < nf && e == cudaSuccess; f0 += chunk, ++i) {
+    const int sl = i % ring;
+    const int64_t n = std::min<int64_t>(chunk, nf - f0);
+    void* W = (char*)ws + sl * slot_bytes;
+    if (i >= ring) cudaStreamWaitEvent(f.sa, f.ev_rows[sl], 0);  // slot consumed by rows(i - ring)
+    e = f.dtype == GRFC_F64 ? launch_cols_any<double>(f, alg, seed, field0 + f0, n, W, f.sa)
+                            : launch_cols_any<float>(f, alg, seed, field0 + f0, n, W, f.sa);
+    if (e != cudaSuccess) break;
+    cudaEventRecord(f.ev_cols[sl], f.sa);
+    cudaStreamWaitEvent(f.sb, f.ev_cols[sl], 0);
+    char* o = (char*)out + f0 * stride * esz;
+    e = f.dtype == GRFC_F64 ? dispatch_rows<double>(f, n, W, o, stride, f.sb)
+                            : dispatch_rows<float>(f, n, W, o, stride, f.sb);
+    cudaEventRecord(f.ev_rows[sl], f.sb);
+  }
+  cudaEventRecord(f.ev_ja, f.sa);
+  cudaEventRecord(f.ev_jb, f.sb);
+  cudaStreamWaitEvent(s, f.ev_ja, 0);
+  cudaStreamWaitEvent(s, f.ev_jb, 0);
+  cudaFreeAsync(ws, s);
+  return e;
 }
 
 cudaError_t launch_fast2d(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,

@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libgrfc.so")
+LIB_PATH = os.environ.get("GRFC_LIB") or os.path.join(_HERE, "lib", "libgrfc.so")
 
 OK, EINVAL, ERUNTIME, ECUDA, ENCCL = 0, 1, 2, 3, 4
 F32, F64 = 0, 1
@@ -221,7 +221,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:
             _lib.grfc_plan_destroy(h)
             self._h = C.c_void_p(None)
 

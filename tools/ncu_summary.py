@@ -1,0 +1,40 @@
+"""Summarise an ncu report: SOL, occupancy, IPC, stall reasons, pipe use, DRAM bytes.
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "sm__inst_executed.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "sm__cycles_active.avg", "gpc__cycles_elapsed.max",
+]
+
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        print("==", d.get("Kernel Name", "")[:100])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:70s} {d[k]}")
+        stalls = {k: d[k] for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
+        tot = sum(float(v or 0) for v in stalls.values())
+        for k, v in sorted(stalls.items(), key=lambda kv: -float(kv[1] or 0))[:8]:
+            print(f"  stall {k[len('smsp__pcsamp_warps_issue_stalled_'):]:40s} {100 * float(v or 0) / max(tot, 1):5.1f}%")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
