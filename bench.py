@@ -196,6 +196,7 @@ def kernel_alg_bytes(name, P, H, s):
         "c2r_last": H * c + P * s,          # read half spectrum, write field
         "fused_rows_c2r": P * s + P * s,    # read packed spectrum (P/2 complex), write field
         "fused_cols_gen": P * s,            # write packed column-transformed spectrum
+        "fused2d_persistent": P * s,        # whole path in one kernel: compulsory field write only
         "gen_half": H * c,
         "line_c2c": 2 * H * c,
         "r2c_last_noise": H * c,

@@ -91,6 +91,13 @@ grfc_status grfc_count_draws(int dim, const int64_t* counts, int algorithm, uint
  * grfc_plan_set_sqrt_gamma_table expects (row-major over H). */
 grfc_status grfc_half_lattice_cells(int dim, const int64_t* counts, uint64_t* out);
 
+/* Representative set of the lattice in the paper-Appendix order — the
+ * reference's for_each_conjugate_rep (src/hermitian.cpp:39-84,308-311) and the
+ * Alg-3 draw order: row-major linear index and self-conjugate flag of each
+ * rep, written up to `cap` entries; *count = |L| = 2^d + (P - 2^d)/2. */
+grfc_status grfc_conjugate_reps(int dim, const int64_t* counts, int64_t* lin, uint8_t* self_flag, uint64_t cap,
+                                uint64_t* count);
+
 /* Plan = GridSpec (include/grf/grid.hpp:16-47, validated as src/grid.cpp:10-30)
  * + density + algorithm + precision, bound to one device. Replaces the
  * per-call setup of grf::synthesize (src/synth.cpp:68-80) and the FFTW plan
@@ -129,6 +136,10 @@ grfc_status grfc_generate_host(grfc_plan plan, uint64_t seed, uint64_t first_fie
 grfc_status grfc_generate_injected(grfc_plan plan, const double* draws, uint64_t ndraws,
                                    void* d_out, void* stream);
 
+/* grfc_generate_injected with a HOST output buffer (P elements of the plan's
+ * dtype); synchronous. What the C++ drop-in's stream overload calls. */
+grfc_status grfc_generate_injected_host(grfc_plan plan, const double* draws, uint64_t ndraws, void* h_out);
+
 /* Host-only noise bridge (no device): the unit-variance Hermitian noise w(K)
  * the reference would assemble from `draws` (its own draw order) for every
  * half-lattice cell K, row-major over H, interleaved (re, im) — i.e. the
@@ -150,6 +161,10 @@ grfc_status grfc_dump_noise(grfc_plan plan, uint64_t seed, uint64_t field, doubl
  * device pointers, out-of-place (in == out rejected as src/dft.cpp:21-22). */
 grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, double* d_out,
                          int sign, void* stream);
+/* Same with host buffers on `device` (synchronous): the CudaDftBackend of
+ * the C++ drop-in (replaces FftwBackend::forward/inverse, src/dft.cpp:95-108). */
+grfc_status grfc_dft_c2c_host(int dim, const int64_t* counts, const double* h_in, double* h_out, int sign,
+                              int device);
 
 /* Plan introspection for benchmarks: bytes of workspace per field and the
  * kernel path chosen ("pow2-2d", "generic", ...). */

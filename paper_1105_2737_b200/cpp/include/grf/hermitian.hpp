@@ -1,0 +1,40 @@
+// grf Hermitian-spectrum helpers — drop-in for the reference's
+// include/grf/hermitian.hpp (host-side utilities; the generator assembles its
+// spectrum on the device).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <functional>
+#include <vector>
+
+#include "grf/grid.hpp"
+#include "grf/random.hpp"
+#include "grf/spectral.hpp"
+
+namespace grf {
+
+struct ConjugateRepSet {
+  GridSpec grid;
+  std::vector<MultiIndex> reps;            // L0 first, then the Appendix blocks
+  std::vector<MultiIndex> self_conjugate;  // the 2^d entries of L0
+};
+
+/// Representative set in the paper-Appendix order (the Alg-3 draw order).
+ConjugateRepSet build_conjugate_reps(const GridSpec& grid);
+void for_each_conjugate_rep(const GridSpec& grid, const std::function<void(const MultiIndex&, bool)>& fn);
+
+struct HermitianSpectrum {
+  GridSpec grid;
+  std::vector<std::complex<double>> values;  // P entries, row-major
+};
+
+enum class SpectrumMode { exact_set, overwrite };
+
+/// V(K) = sqrt(g(w_K)) w(K) on the full lattice from draws pulled from rng.
+HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
+                                      SpectrumMode mode);
+bool verify_hermitian(const HermitianSpectrum& spectrum);
+std::uint64_t spectrum_draw_count(const GridSpec& grid, SpectrumMode mode);
+
+}  // namespace grf

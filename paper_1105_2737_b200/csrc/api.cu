@@ -297,6 +297,25 @@ grfc_status grfc_half_lattice_cells(int dim, const int64_t* counts, uint64_t* ou
   return GRFC_OK;
 }
 
+grfc_status grfc_conjugate_reps(int dim, const int64_t* counts, int64_t* lin, uint8_t* self_flag, uint64_t cap,
+                                uint64_t* count) {
+  std::string err;
+  if (!counts || !count || (cap && (!lin || !self_flag))) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!validate_grid(dim, counts, nullptr, err)) return fail(GRFC_EINVAL, err);
+  uint64_t i = 0;
+  for_each_rep(dim, counts, [&](const int64_t* k, bool self) {
+    if (i < cap) {
+      int64_t l = 0;
+      for (int a = 0; a < dim; ++a) l = l * counts[a] + k[a];
+      lin[i] = l;
+      self_flag[i] = self ? 1 : 0;
+    }
+    ++i;
+  });
+  *count = i;
+  return GRFC_OK;
+}
+
 grfc_status grfc_half_noise_from_draws(int dim, const int64_t* counts, int algorithm, const double* draws,
                                        uint64_t ndraws, double* w_half) {
   std::string err;
@@ -629,6 +648,48 @@ grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, dou
   }
   if (sign < 0) GRFC_CUDA(launch_scale_all<double>(d_out, P, 1.0 / (double)P, s));
   return GRFC_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+grfc_status grfc_generate_injected_host(grfc_plan p, const double* draws, uint64_t ndraws, void* h_out) {
+  if (!p || !h_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  DeviceGuard guard(p->device);
+  void* d = nullptr;
+  GRFC_CUDA(cudaMalloc(&d, p->points * dsize(p)));
+  grfc_status st = grfc_generate_injected(p, draws, ndraws, d, nullptr);
+  if (st == GRFC_OK) {
+    cudaError_t e = cudaMemcpy(h_out, d, p->points * dsize(p), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(GRFC_ECUDA, std::string("CUDA: D2H: ") + cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return st;
+}
+
+grfc_status grfc_dft_c2c_host(int dim, const int64_t* counts, const double* h_in, double* h_out, int sign,
+                              int device) {
+  if (!counts || !h_in || !h_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (h_in == h_out) return fail(GRFC_EINVAL, "DftBackend: in-place transform not supported");
+  if (dim < 1 || dim > GRFC_MAX_DIM) return fail(GRFC_EINVAL, "grfc: bad dimension");
+  int64_t P = 1;
+  for (int a = 0; a < dim; ++a) P *= counts[a];
+  DeviceGuard guard(device);
+  double *din = nullptr, *dout = nullptr;
+  GRFC_CUDA(cudaMalloc(&din, (size_t)P * 16));
+  cudaError_t e = cudaMalloc(&dout, (size_t)P * 16);
+  if (e == cudaSuccess) e = cudaMemcpy(din, h_in, (size_t)P * 16, cudaMemcpyHostToDevice);
+  grfc_status st = GRFC_OK;
+  if (e != cudaSuccess) st = fail(GRFC_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e));
+  if (st == GRFC_OK) st = grfc_dft_c2c(dim, counts, din, dout, sign, nullptr);
+  if (st == GRFC_OK) {
+    e = cudaMemcpy(h_out, dout, (size_t)P * 16, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(GRFC_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e));
+  }
+  cudaFree(din);
+  cudaFree(dout);
+  return st;
 }
 
 }  // extern "C"

@@ -109,6 +109,9 @@ def _load():
         "grfc_plan_info": [P, P, P, P],
         "grfc_half_noise_from_draws": [C.c_int, P, C.c_int, P, C.c_uint64, P],
         "grfc_kernel_timing_read": [C.c_int, P, P, P],
+        "grfc_generate_injected_host": [P, P, C.c_uint64, P],
+        "grfc_dft_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
+        "grfc_conjugate_reps": [C.c_int, P, P, P, C.c_uint64, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -129,7 +132,19 @@ EXPORTED = (
     "grfc_plan_set_sqrt_gamma_table", "grfc_plan_destroy", "grfc_generate", "grfc_generate_host",
     "grfc_generate_injected", "grfc_half_noise_from_draws", "grfc_dump_noise", "grfc_dft_c2c", "grfc_plan_info",
     "grfc_last_launch_count", "grfc_kernel_timing_enable", "grfc_kernel_timing_read",
+    "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps",
 )
+
+
+def conjugate_reps(counts: Sequence[int]):
+    """(linear indices, self-conjugate flags) of the representative set, Appendix order."""
+    P = int(np.prod(counts))
+    lin = np.zeros(P, np.int64)
+    flg = np.zeros(P, np.uint8)
+    n = C.c_uint64(0)
+    _check(_lib.grfc_conjugate_reps(len(counts), _i64(counts), lin.ctypes.data_as(C.c_void_p),
+                                    flg.ctypes.data_as(C.c_void_p), P, C.byref(n)))
+    return lin[: n.value], flg[: n.value].astype(bool)
 
 
 def kernel_timing_enable(on: bool):
