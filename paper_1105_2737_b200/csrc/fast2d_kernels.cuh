@@ -411,7 +411,9 @@ template <int N1, int M, typename T>
 constexpr int rows_per_tile() {
   constexpr int teams = fused_threads<N1, M, T>() / (M / RowPlan<M, T>::E);
   constexpr int cap = (int)(200 * 1024 / (row_pitch<M, C_t<T>>() * sizeof(C_t<T>)));
-  return teams < cap ? teams : cap;
+  int p2 = 1;  // power of two, so tiles divide N1 exactly
+  while (2 * p2 <= cap) p2 *= 2;
+  return teams < p2 ? teams : p2;
 }
 template <int N1, int M, typename T>
 constexpr size_t fused_smem() {
