@@ -21,6 +21,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -307,12 +309,19 @@ __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
 }
 
 // ---------------------------------------------------------------- tiles
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
 // generation fused in front and the Z epilogue behind. Block = col_threads.
 template <typename T, int N1, int ALG>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
-                                         unsigned char* smem_raw) {
+                                         unsigned char* smem_raw, const float* __restrict__ rowq,
+                                         const uint32_t* dep = nullptr, uint32_t dep_target = 0) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -324,10 +333,34 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // Generation into shared memory (rolled loop: one copy of the Philox/Box-
   // Muller/density code in the I-cache). Thread j owns rows j + t*TT.
   C* sm = reinterpret_cast<C*>(smem_raw);
-  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
-    // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one Philox call
-    const T r = (T)0.70710678118654752440, sc = (T)p.scale;
+  // Thread 0 reads the slot's "previous rows consumed" counter now (relaxed);
+  // it is only needed before the W stores, so its latency hides behind the tile.
+  uint32_t dep_seen = 0;
+  if (dep && threadIdx.x == 0) dep_seen = ld_relaxed_u32(dep);
+  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
+    // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one
+    // Philox call. sqrt(g) from the per-CTA row table rowq (fused2d_row_table):
+    //   Matern   rowq = ell^2 w1^2:      m = K ex2(-alpha/2 lg2(A_col + rowq))
+    //   Gaussian rowq = ex2(-ell^2 w1^2/4 log2 e):  m = B_col rowq
+    const int k2w = col <= p.n2 / 2 ? col : col - p.n2;
+    const float w2 = (float)k2w * p.f_wstep2;
+    const float K = p.f_sqrt_c * p.f_scale * 0.70710678118654752440f;
+    const bool matern = p.family == GRFC_DENSITY_MATERN;
+    const float A = 1.0f + p.f_ell2 * w2 * w2, B = K * ex2_approx(p.f_gauss_k * w2 * w2);
 #pragma unroll 2
+    for (int t = 0; t < E / 2; ++t) {
+      const int k1 = j + t * TT;
+      float a0, b0, a1, b1;
+      unit_quad_f32(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col), a0, b0, a1, b1);
+      const float q0 = rowq[k1], q1 = rowq[k1 + N1 / 2];
+      const float m0 = matern ? K * ex2_approx(p.f_nhalf_alpha * lg2_approx(A + q0)) : B * q0;
+      const float m1 = matern ? K * ex2_approx(p.f_nhalf_alpha * lg2_approx(A + q1)) : B * q1;
+      sm[k1 * SLOTS + slot] = mk<C>((T)(a0 * m0), (T)(-b0 * m0));
+      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(a1 * m1), (T)(-b1 * m1));
+    }
+  } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
+    const T r = (T)0.70710678118654752440, sc = (T)p.scale;
+#pragma unroll 1
     for (int t = 0; t < E / 2; ++t) {
       const int k1 = j + t * TT;
       float a0, b0, a1, b1;
@@ -358,7 +391,14 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   ColEx<C, SLOTS> ex{sm, slot};
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
 
+  // The slot's previous field must be consumed before W is overwritten.
+  if (dep) {
+    if (threadIdx.x == 0 && dep_seen < dep_target)
+      while (ld_relaxed_u32(dep) < dep_target) __nanosleep(256);
+    __syncthreads();
+  }
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
+  const bool special = packed || mid;
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -368,8 +408,29 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       P.x = __shfl_xor_sync(0xffffffffu, v[e].x, CB);
       P.y = __shfl_xor_sync(0xffffffffu, v[e].y, CB);
       const int row = j + b * TT + i * (N1 / RL);
-      __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], P, packed, mid, w));
+      if (!special) __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], P, false, false, w));
     }
+  if (special) {
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) {
+        const int e = b * RL + i;
+        const int row = j + b * TT + i * (N1 / RL);
+        __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], v[e], packed, mid, w));
+      }
+  }
+}
+
+// Per-CTA row table of the fp32 fused density path (see col_tile).
+template <int N1>
+__device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq) {
+  for (int k1 = threadIdx.x; k1 < N1; k1 += blockDim.x) {
+    const int k1w = k1 <= p.n1 / 2 ? k1 : k1 - p.n1;
+    const float w1 = (float)k1w * p.f_wstep1;
+    rowq[k1] = p.family == GRFC_DENSITY_MATERN ? p.f_ell2 * w1 * w1 : ex2_approx(p.f_gauss_k * w1 * w1);
+  }
+  __syncthreads();
 }
 
 // Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
@@ -437,17 +498,13 @@ struct F2Sched {
   uint32_t* col_done;  // [S]
   uint32_t* row_done;  // [S]
   uint32_t F, L, S, strips, rtiles;
+  // GRFC_TILE_STATS=1: per-launch cycle counters [col, row, col-wait, row-wait, ticket, ncol, nrow]
+  unsigned long long* stats;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -470,20 +527,43 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
   }
 }
 
+// Resident CTAs per SM the fused kernel is compiled for (register budget):
+// tuned for the c2 shape (fp32 512 columns: 3 x 256 threads at 80 registers,
+// no spills); other shapes let ptxas choose.
+#ifndef GRFC_FUSED_MINB
+#define GRFC_FUSED_MINB 3
+#endif
+template <int N1, int M, typename T>
+constexpr int fused_min_blocks() {
+  return (N1 == 512 && sizeof(T) == 4) ? GRFC_FUSED_MINB : 0;
+}
 template <typename T, int N1, int M, int ALG>
-__global__ void __launch_bounds__(fused_threads<N1, M, T>())
+__global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1, M, T>())
     k_fused2d(F2Params p, F2Sched q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring, T* __restrict__ out,
               int64_t out_stride, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
+  __shared__ float s_rowq[N1];
   constexpr int RPT = rows_per_tile<N1, M, T>();
+  const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
+  if (table) fused2d_row_table<N1>(p, s_rowq);
+  // Thread 0 keeps one ticket in flight: the atomic for tile i+1 is issued
+  // when tile i starts, so its round trip overlaps tile i.
+  uint32_t next_ticket = 0;
+  if (threadIdx.x == 0) next_ticket = atomicAdd(q.ticket, 1u);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
   const uint32_t total = q.F * G;
+  long long c_col = 0, c_row = 0, c_wc = 0, c_wr = 0, c_tk = 0, n_col = 0, n_row = 0;
   for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(q.ticket, 1u);
+    long long t0 = q.stats ? clock64() : 0;
+    if (threadIdx.x == 0) {
+      s_ticket = next_ticket;
+      if (next_ticket < total) next_ticket = atomicAdd(q.ticket, 1u);
+    }
     __syncthreads();
     uint32_t t = s_ticket;
+    if (q.stats) c_tk += clock64() - t0;
     if (t >= total) break;
     bool col;
     uint32_t f, idx;
@@ -505,14 +585,37 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>())
     const uint32_t slot = f % q.S, use = f / q.S;
     C_t<T>* Wf = ring + slot * slot_elems;
     if (col) {
-      wait_geq(&q.row_done[slot], use * q.rtiles);
-      col_tile<T, N1, ALG>(p, key, field0 + f, (int)idx, Wf, tw1, tw2, smem_raw);
+      long long a = q.stats ? clock64() : 0;
+      long long b = a;
+      col_tile<T, N1, ALG>(p, key, field0 + f, (int)idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
+                           use ? &q.row_done[slot] : nullptr, use * q.rtiles);
       signal_done(&q.col_done[slot]);
+      if (q.stats) {
+        c_wc += b - a;
+        c_col += clock64() - b;
+        ++n_col;
+      }
     } else {
+      long long a = q.stats ? clock64() : 0;
       wait_geq(&q.col_done[slot], (use + 1) * q.strips);
+      long long b = q.stats ? clock64() : 0;
       row_tile<T, M, RPT>(Wf, (int)idx * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw);
       signal_done(&q.row_done[slot]);
+      if (q.stats) {
+        c_wr += b - a;
+        c_row += clock64() - b;
+        ++n_row;
+      }
     }
+  }
+  if (q.stats && threadIdx.x == 0) {
+    atomicAdd(&q.stats[0], (unsigned long long)c_col);
+    atomicAdd(&q.stats[1], (unsigned long long)c_row);
+    atomicAdd(&q.stats[2], (unsigned long long)c_wc);
+    atomicAdd(&q.stats[3], (unsigned long long)c_wr);
+    atomicAdd(&q.stats[4], (unsigned long long)c_tk);
+    atomicAdd(&q.stats[5], (unsigned long long)n_col);
+    atomicAdd(&q.stats[6], (unsigned long long)n_row);
   }
 }
 
@@ -523,10 +626,14 @@ __global__ void __launch_bounds__(col_threads<N1, T>())
     k_cols_gen(F2Params p, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ W,
                const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ float s_rowq[N1];
+  const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
+  if (table) fused2d_row_table<N1>(p, s_rowq);
   const int strips = p.m / (2 * ColPlan<N1, T>::X);
   const int s = (int)(blockIdx.x % (unsigned)strips);
   const uint64_t f = blockIdx.x / (unsigned)strips;
-  col_tile<T, N1, ALG>(p, key, field0 + f, s, W + f * (uint64_t)N1 * (uint64_t)p.m, tw1, tw2, smem_raw);
+  col_tile<T, N1, ALG>(p, key, field0 + f, s, W + f * (uint64_t)N1 * (uint64_t)p.m, tw1, tw2, smem_raw,
+                       table ? s_rowq : nullptr);
 }
 
 template <typename T, int M>
@@ -649,9 +756,31 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   const C* tw2 = tw1 + f.n1;
   const uint32_t total = q.F * (q.strips + q.rtiles);
   const uint32_t grid = total < conc ? total : conc;
-  LaunchScope ls("fused2d_persistent", s);
-  k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(make_params(f), q, philox_key(seed), field0, ring, (T*)out, stride, tw1, tw2);
-  return cudaGetLastError();
+  const char* st = std::getenv("GRFC_TILE_STATS");
+  unsigned long long* dstats = nullptr;
+  if (st && st[0] == '1') {
+    cudaMalloc(&dstats, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(dstats, 0, 8 * sizeof(unsigned long long), s);
+  }
+  q.stats = dstats;
+  {
+    LaunchScope ls("fused2d_persistent", s);
+    k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(make_params(f), q, philox_key(seed), field0, ring, (T*)out, stride,
+                                                    tw1, tw2);
+  }
+  e = cudaGetLastError();
+  if (dstats) {
+    unsigned long long h[8] = {};
+    cudaMemcpyAsync(h, dstats, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(dstats);
+    const double nc = (double)(h[5] ? h[5] : 1), nr = (double)(h[6] ? h[6] : 1);
+    std::fprintf(stderr,
+                 "[grfc tile stats] grid=%u L=%u S=%u | col tiles %llu: %.0f cyc/tile, wait %.0f | row tiles %llu: "
+                 "%.0f cyc/tile, wait %.0f | ticket %.0f cyc/tile\n",
+                 grid, q.L, q.S, h[5], h[0] / nc, h[2] / nc, h[6], h[1] / nr, h[3] / nr, h[4] / (nc + nr));
+  }
+  return e;
 }
 
 }  // namespace grfc
