@@ -166,6 +166,27 @@ grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, dou
 grfc_status grfc_dft_c2c_host(int dim, const int64_t* counts, const double* h_in, double* h_out, int sign,
                               int device);
 
+/* Slab decomposition of one 3D field over `world` ranks (pow2 3D plans;
+ * world divides N0 and N1) — the multi-GPU form of grfc_generate for a
+ * single large field. Per field and rank:
+ *   grfc_slab_pass_a  generation + axis-0 FFT of the rank's spectrum slab
+ *                     (k1 in [rank N1/world, (rank+1) N1/world)) into d_send;
+ *   all-to-all        block q of every rank's d_send (elements
+ *                     [q*block, (q+1)*block), complex) goes to block r of
+ *                     rank q's d_recv — contiguous blocks, no packing (NCCL
+ *                     ncclAlltoAll / grouped ncclSend-ncclRecv, or
+ *                     torch.distributed.all_to_all_single);
+ *   grfc_slab_pass_b  axis-1 + axis-2 transforms of the rank's field planes
+ *                     j0 in [rank N0/world, ...) into d_out (slab_points reals).
+ * Mirror partners that live on other ranks are regenerated locally from the
+ * counter-based noise, never exchanged. Results are bit-identical for every
+ * world size. Buffer sizes are in complex elements of the plan's dtype. */
+grfc_status grfc_slab_sizes(grfc_plan plan, int world, uint64_t* buf_elems, uint64_t* block_elems,
+                            uint64_t* slab_points);
+grfc_status grfc_slab_pass_a(grfc_plan plan, int world, int rank, uint64_t seed, uint64_t field, void* d_send,
+                             void* stream);
+grfc_status grfc_slab_pass_b(grfc_plan plan, int world, const void* d_recv, void* d_out, void* stream);
+
 /* Plan introspection for benchmarks: bytes of workspace per field and the
  * kernel path chosen ("pow2-2d", "generic", ...). */
 grfc_status grfc_plan_info(grfc_plan plan, uint64_t* cells_half, uint64_t* points,

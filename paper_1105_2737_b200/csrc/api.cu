@@ -14,6 +14,7 @@
 
 #include "../../include/grfc.h"
 #include "fast2d.h"
+#include "fast3d.h"
 #include "grfc_internal.cuh"
 #include "host_lattice.h"
 #include "kernels.h"
@@ -138,6 +139,8 @@ struct grfc_plan_s {
   double s_two = 1.0;  // Alg 1:   sqrt((2 pi)^d P / |A|) / P   (synth.cpp:89-90 + dft.cpp:106)
   bool fast = false;
   Fast2D fast2d{};
+  bool fast3 = false;
+  Fast3D fast3d{};
   std::string path = "generic";
 
   const void* tw(int a) const { return (const char*)d_tw + tw_off[a] * csize; }
@@ -420,6 +423,12 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
     p->fast = true;
     p->path = fast2d_name(p->fast2d);
   }
+  if (allow_fast && fast3d_supported(dim, counts, algorithm)) {
+    cudaError_t e = fast3d_init(p->fast3d, p->g, p->D, dtype, algorithm, p->s_one);
+    if (e != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: fast3d_init: ") + cudaGetErrorString(e));
+    p->fast3 = true;
+    p->path = dtype == GRFC_F64 ? "pow2-3d-f64" : "pow2-3d-f32";
+  }
   *out = p.release();
   return GRFC_OK;
 }
@@ -434,6 +443,7 @@ grfc_status grfc_plan_set_sqrt_gamma_table(grfc_plan p, const double* sg) {
   GRFC_CUDA(cudaMemcpy(p->d_table, sg, p->cells * sizeof(double), cudaMemcpyHostToDevice));
   p->D.table = p->d_table;
   if (p->fast) p->fast2d.D.table = p->d_table;
+  if (p->fast3) p->fast3d.D.table = p->d_table;
   p->table_set = true;
   return GRFC_OK;
 }
@@ -442,6 +452,7 @@ void grfc_plan_destroy(grfc_plan p) {
   if (!p) return;
   DeviceGuard guard(p->device);
   if (p->fast) fast2d_free(p->fast2d);
+  if (p->fast3) fast3d_free(p->fast3d);
   cudaFree(p->d_tw);
   cudaFree(p->d_table);
   delete p;
@@ -465,6 +476,11 @@ grfc_status grfc_generate(grfc_plan p, uint64_t seed, uint64_t first_field, uint
   if (nfields == 0) return GRFC_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->fast3 && field_stride % 2 == 0) {  // fused pow2 3D path (pow2_3d.cu)
+    cudaError_t e = fast3d_generate(p->fast3d, seed, first_field, (int64_t)nfields, d_out, (int64_t)field_stride, s);
+    if (e != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: fused3d: ") + cudaGetErrorString(e));
+    return GRFC_OK;
+  }
   // Fused pow2 2D path: whole batch, pipelined internally (pow2_2d.cu).
   if (p->fast && field_stride % 2 == 0) {
     cudaError_t e = fast2d_generate(p->fast2d, p->alg, seed, first_field, (int64_t)nfields, d_out,
@@ -690,6 +706,46 @@ grfc_status grfc_dft_c2c_host(int dim, const int64_t* counts, const double* h_in
   cudaFree(din);
   cudaFree(dout);
   return st;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+grfc_status grfc_slab_sizes(grfc_plan p, int world, uint64_t* buf_elems, uint64_t* block_elems,
+                            uint64_t* slab_points) {
+  if (!p) return fail(GRFC_EINVAL, "grfc: null plan");
+  if (!p->fast3) return fail(GRFC_EINVAL, "grfc: slab decomposition needs a pow2 3D plan");
+  SlabGeom g;
+  if (!slab_geometry(p->fast3d, world, g)) return fail(GRFC_EINVAL, "grfc: world must divide N0 and N1");
+  if (buf_elems) *buf_elems = g.buf_elems;
+  if (block_elems) *block_elems = g.block_elems;
+  if (slab_points) *slab_points = (uint64_t)g.n0p * p->n[1] * p->n[2];
+  return GRFC_OK;
+}
+
+grfc_status grfc_slab_pass_a(grfc_plan p, int world, int rank, uint64_t seed, uint64_t field, void* d_send,
+                             void* stream) {
+  t_launches = 0;
+  if (!p || !d_send) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!p->fast3) return fail(GRFC_EINVAL, "grfc: slab decomposition needs a pow2 3D plan");
+  SlabGeom g;
+  if (!slab_geometry(p->fast3d, world, g) || rank < 0 || rank >= world)
+    return fail(GRFC_EINVAL, "grfc: bad world/rank for this grid");
+  DeviceGuard guard(p->device);
+  GRFC_CUDA(fast3d_pass_a(p->fast3d, world, rank, seed, field, d_send, (cudaStream_t)stream));
+  return GRFC_OK;
+}
+
+grfc_status grfc_slab_pass_b(grfc_plan p, int world, const void* d_recv, void* d_out, void* stream) {
+  t_launches = 0;
+  if (!p || !d_recv || !d_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (!p->fast3) return fail(GRFC_EINVAL, "grfc: slab decomposition needs a pow2 3D plan");
+  SlabGeom g;
+  if (!slab_geometry(p->fast3d, world, g)) return fail(GRFC_EINVAL, "grfc: world must divide N0 and N1");
+  DeviceGuard guard(p->device);
+  GRFC_CUDA(fast3d_pass_b(p->fast3d, world, d_recv, d_out, (cudaStream_t)stream));
+  return GRFC_OK;
 }
 
 }  // extern "C"

@@ -36,8 +36,9 @@ struct Fast2D {
 
 // Lookahead L (fields of column work ahead of row work) and ring slots S for
 // a batch of nf fields; conc = resident CTAs.
-inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S, uint32_t* conc) {
-  const uint32_t c = (uint32_t)(f.sms * f.occ), G = (uint32_t)(f.strips + f.rtiles);
+inline void ring_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, uint32_t* L, uint32_t* S,
+                          uint32_t* conc) {
+  const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + rtiles);
   uint32_t l = (4 * c + G - 1) / G;
   l = l < 1 ? 1 : l;
   l = l < (uint32_t)nf ? l : (uint32_t)nf;
@@ -46,6 +47,9 @@ inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S
   *L = l;
   *S = s;
   *conc = c;
+}
+inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S, uint32_t* conc) {
+  ring_geometry(f.sms, f.occ, f.strips, f.rtiles, nf, L, S, conc);
 }
 inline size_t fused_ctr_bytes(uint32_t S) { return ((1 + 2 * (size_t)S) * 4 + 255) / 256 * 256; }
 // Device workspace one persistent launch over nf fields needs.

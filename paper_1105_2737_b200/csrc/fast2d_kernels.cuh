@@ -71,6 +71,7 @@ struct RowPlan {
     static constexpr int X = X_;           \
     using R = Radices<__VA_ARGS__>;        \
   };
+GRFC_PLAN(ColPlan, 128, float, 16, 4, 16, 8)
 GRFC_PLAN(ColPlan, 256, float, 16, 8, 16, 16)
 #ifndef GRFC_COL512
 #define GRFC_COL512 2
@@ -87,16 +88,19 @@ GRFC_PLAN(ColPlan, 512, float, 32, 8, 32, 16)
 GRFC_PLAN(ColPlan, 1024, float, 32, 8, 32, 32)
 GRFC_PLAN(ColPlan, 2048, float, 16, 4, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, float, 16, 2, 16, 16, 16)
+GRFC_PLAN(ColPlan, 128, double, 16, 4, 16, 8)
 GRFC_PLAN(ColPlan, 256, double, 16, 8, 16, 16)
 GRFC_PLAN(ColPlan, 512, double, 16, 8, 16, 16, 2)
 GRFC_PLAN(ColPlan, 1024, double, 16, 4, 16, 16, 4)
 GRFC_PLAN(ColPlan, 2048, double, 16, 2, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, double, 16, 1, 16, 16, 16)
+GRFC_PLAN(RowPlan, 64, float, 8, 16, 8, 8)
 GRFC_PLAN(RowPlan, 128, float, 16, 16, 16, 8)
 GRFC_PLAN(RowPlan, 256, float, 16, 16, 16, 16)
 GRFC_PLAN(RowPlan, 512, float, 32, 16, 32, 16)
 GRFC_PLAN(RowPlan, 1024, float, 32, 8, 32, 32)
 GRFC_PLAN(RowPlan, 2048, float, 16, 2, 16, 16, 8)
+GRFC_PLAN(RowPlan, 64, double, 8, 16, 8, 8)
 GRFC_PLAN(RowPlan, 128, double, 16, 16, 16, 8)
 GRFC_PLAN(RowPlan, 256, double, 16, 16, 16, 16)
 GRFC_PLAN(RowPlan, 512, double, 16, 8, 16, 16, 2)

@@ -1,0 +1,279 @@
+// Fused power-of-two 3D path (BASELINE config c4: 512^3 fp32, Algorithm 2),
+// single GPU and slab-decomposed across ranks.
+//
+// Formulation. With M = N2/2, the field is the plain complex FFT (exp(+), all
+// axes) of the "pre-twiddled" half spectrum over (N0, N1, M):
+//   Zh(k0,k1,k) = (X(k0,k1,k) + conj X(-k0,-k1,M-k))
+//               + i e^{2 pi i k/N2} (X(k0,k1,k) - conj X(-k0,-k1,M-k)),
+//   z = FFT+_{N0,N1,M}(Zh),  field(j0,j1,2m) + i field(j0,j1,2m+1) = z(j0,j1,m),
+// (the last-axis half-complex -> real pre-twiddle, moved in front of the
+// other axes' transforms: conj(FFT(y)) = FFT(conj(y(-k)))). X = conj(V) * scale
+// is the reference spectrum (hermitian.cpp:128-203), evaluated cell by cell.
+//
+// Pass A  k_3d_colgen   tile = (k1 pair {k1, -k1}, strip of 2*CB columns k):
+//         generates X for the 4*CB columns {k1,-k1} x {k, M-k} (+ the Nyquist
+//         column M where k = 0), forms Zh with its fully mirrored partner via
+//         shared memory, FFTs along axis 0, stores W[j0][k1 - k1_lo][k] for
+//         the k1 of this rank's slab.
+// (exchange) slab all-to-all: block q of rank r = W_r[j0 in slab q] — a
+//         contiguous range, no packing.
+// Pass B  k_3d_planes   persistent: per plane j0, column tiles (axis-1 FFT,
+//         reading the received blocks) then row tiles (axis-2 FFT = row_tile,
+//         writing the field rows); planes go through an L2 ring like the 2D
+//         fused kernel.
+#pragma once
+
+#include "fast2d_kernels.cuh"
+
+namespace grfc {
+
+// Pass-A plan: E elements per thread, CB columns per side, radices.
+template <int N, typename T>
+struct ColPlan3 {
+  static constexpr int E = 0;
+};
+#define GRFC_PLAN3(N, TT, E_, X_, ...) \
+  template <>                          \
+  struct ColPlan3<N, TT> {             \
+    static constexpr int E = E_;       \
+    static constexpr int X = X_;       \
+    using R = Radices<__VA_ARGS__>;    \
+  };
+GRFC_PLAN3(128, float, 16, 4, 16, 8)
+GRFC_PLAN3(256, float, 16, 4, 16, 16)
+GRFC_PLAN3(512, float, 16, 4, 16, 16, 2)
+GRFC_PLAN3(1024, float, 16, 4, 16, 16, 4)
+GRFC_PLAN3(128, double, 16, 2, 16, 8)
+GRFC_PLAN3(256, double, 16, 2, 16, 16)
+GRFC_PLAN3(512, double, 16, 2, 16, 16, 2)
+GRFC_PLAN3(1024, double, 16, 2, 16, 16, 4)
+#undef GRFC_PLAN3
+
+template <int N0, typename T>
+constexpr int colgen3_threads() {
+  return 4 * ColPlan3<N0, T>::X * (N0 / ColPlan3<N0, T>::E);
+}
+
+struct F3Params {
+  int n0, n1, n2, m, hd;  // hd = M + 1
+  double wstep[3];
+  float f_wstep[3], f_sqrt_c, f_ell2, f_nhalf_alpha, f_gauss_k, f_scale;
+  double sqrt_c, alpha, ell, scale;
+  uint64_t uh;
+  int family, alg;
+  DensityDesc D;
+  GridDesc g;
+};
+
+template <typename T>
+__device__ __forceinline__ T sqrt_g3(const F3Params& p, int k0, int k1, int k2) {
+  const int w0i = k0 <= p.n0 / 2 ? k0 : k0 - p.n0, w1i = k1 <= p.n1 / 2 ? k1 : k1 - p.n1,
+            w2i = k2 <= p.n2 / 2 ? k2 : k2 - p.n2;
+  if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
+    if constexpr (sizeof(T) == 4) {
+      const float a = (float)w0i * p.f_wstep[0], b = (float)w1i * p.f_wstep[1], c = (float)w2i * p.f_wstep[2];
+      const float s = a * a + b * b + c * c;
+      if (p.family == GRFC_DENSITY_GAUSSIAN_COV) return p.f_sqrt_c * ex2_approx(p.f_gauss_k * s);
+      return p.f_sqrt_c * ex2_approx(p.f_nhalf_alpha * lg2_approx(1.0f + p.f_ell2 * s));
+    } else {
+      const double a = w0i * p.wstep[0], b = w1i * p.wstep[1], c = w2i * p.wstep[2];
+      const double s = a * a + b * b + c * c;
+      if (p.family == GRFC_DENSITY_GAUSSIAN_COV) return p.sqrt_c * exp(-0.25 * p.ell * p.ell * s);
+      return p.sqrt_c * pow(1.0 + p.ell * p.ell * s, -0.5 * p.alpha);
+    }
+  }
+  int64_t kw[3] = {w0i, w1i, w2i};
+  return sqrt_gamma<T>(p.g, p.D, kw, ((int64_t)k0 * p.n1 + k1) * p.hd + k2);
+}
+
+// X(K) = conj(w(K)) sqrt(g) scale for any half-lattice cell (generic rules).
+template <typename T>
+__device__ __forceinline__ C_t<T> gen_cell3(const F3Params& p, int k0, int k1, int k2, const PhiloxKey& key,
+                                            uint64_t field) {
+  using C = C_t<T>;
+  const int64_t k[3] = {k0, k1, k2};
+  const int64_t h = ((int64_t)k0 * p.n1 + k1) * p.hd + k2;
+  const C w = philox_cell_noise<T>(p.g, p.alg, k, h, key, field);
+  const T m = sqrt_g3<T>(p, k0, k1, k2) * (T)p.scale;
+  return mk<C>(w.x * m, -w.y * m);
+}
+
+// Pass A. Slots: h in {0: k1, 1: -k1}, side in {L: k, R: M-k}, c < CB;
+// slot = h*2CB + side*CB + c. Zh partner of (h, side, c) is (1-h, 1-side, c);
+// strip 0 exceptions: column 0's partner is the Nyquist column M of -k1 (kept
+// in an extra shared column per h), column M/2's partner is (1-h, R, 0).
+template <typename T, int N0, int ALG>
+__global__ void __launch_bounds__(colgen3_threads<N0, T>(), 1)
+    k_3d_colgen(F3Params p, PhiloxKey key, uint64_t fld, C_t<T>* __restrict__ W, int k1_lo, int k1_cnt,
+                const C_t<T>* __restrict__ tw0, const C_t<T>* __restrict__ tw2) {
+  using C = C_t<T>;
+  using PL = ColPlan3<N0, T>;
+  constexpr int E = PL::E, CB = PL::X, SLOTS = 4 * CB, TT = N0 / E;
+  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  constexpr int PITCH = SLOTS + 2;  // + Nyquist columns of k1 and -k1
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  const int strips = p.m / (2 * CB);
+  const int a = (int)(blockIdx.x / (unsigned)strips), s = (int)(blockIdx.x % (unsigned)strips);
+  const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
+  const int h = slot / (2 * CB), side = (slot / CB) & 1, c = slot % CB;
+  const int k1 = h == 0 ? a : (p.n1 - a) % p.n1;
+  const int kk = s * CB + c;
+  const int col = side == 0 ? kk : (kk == 0 ? p.m / 2 : p.m - kk);
+  const bool zero_col = side == 0 && kk == 0, mid_col = side == 1 && kk == 0;
+
+  // generation (rolled loop): X(k0, k1, col) for k0 = j + t TT
+  const bool fast = ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && col != 0 && col != p.m;
+  if (fast) {
+    // interior column: own draws; rows k0 and k0 + N0/2 are units u and u + Uh
+    const float K = p.f_scale * 0.70710678118654752440f;  // sqrt_g3 includes sqrt(c)
+#pragma unroll 2
+    for (int t = 0; t < E / 2; ++t) {
+      const int k0 = j + t * TT;
+      float a0, b0, a1, b1;
+      unit_quad_f32(key, fld, (uint64_t)(((uint32_t)k0 * p.n1 + k1) * p.hd + col), a0, b0, a1, b1);
+      const float m0 = sqrt_g3<float>(p, k0, k1, col) * K, m1 = sqrt_g3<float>(p, k0 + N0 / 2, k1, col) * K;
+      sm[k0 * PITCH + slot] = mk<C>((T)(a0 * m0), (T)(-b0 * m0));
+      sm[(k0 + N0 / 2) * PITCH + slot] = mk<C>((T)(a1 * m1), (T)(-b1 * m1));
+    }
+  } else {
+#pragma unroll 1
+    for (int t = 0; t < E; ++t) {
+      const int k0 = j + t * TT;
+      sm[k0 * PITCH + slot] = gen_cell3<T>(p, k0, k1, col, key, fld);
+      if (zero_col) sm[k0 * PITCH + SLOTS + h] = gen_cell3<T>(p, k0, k1, p.m, key, fld);
+    }
+  }
+  __syncthreads();
+  // stage-0 inputs: Zh(k0) from X(k0) and the mirrored partner X(-k0)
+  const int pslot = mid_col ? ((1 - h) * 2 * CB + CB) : zero_col ? SLOTS + (1 - h) : ((1 - h) * 2 * CB + (1 - side) * CB + c);
+  const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
+  C v[E];
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) {
+      const int k0 = j + b * TT + i * (N0 / R0);
+      const C X = sm[k0 * PITCH + slot], P = sm[((N0 - k0) & (N0 - 1)) * PITCH + pslot];
+      const C sum = mk<C>(X.x + P.x, X.y - P.y), dif = mk<C>(X.x - P.x, X.y + P.y);
+      const C t = cmul(w, dif);
+      v[b * R0 + i] = mk<C>(sum.x - t.y, sum.y + t.x);
+    }
+  __syncthreads();
+  struct Ex3 {
+    C* s;
+    int slot;
+    __device__ __forceinline__ void put(int e, C x) { s[e * PITCH + slot] = x; }
+    __device__ __forceinline__ C get(int e) const { return s[e * PITCH + slot]; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+  } ex{sm, slot};
+  line_fft<N0, E, +1>(v, j, tw0, 1, ex, typename PL::R{});
+  const int kl = k1 - k1_lo;
+  const bool store = kl >= 0 && kl < k1_cnt && !(h == 1 && k1 == a);  // h = 1 duplicates k1 in {0, N1/2}
+  if (store) {
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) {
+        const int j0 = j + b * TT + i * (N0 / RL);
+        W[((int64_t)j0 * k1_cnt + kl) * p.m + col] = v[b * RL + i];
+      }
+  }
+}
+
+// Plain column tile (axis-1 FFT) of one plane: SLOTS consecutive columns,
+// rows fetched through the slab block layout, output to a ring slot.
+template <typename T, int N1>
+__device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int j0l, int n0_per, int n1_per, int m,
+                                             int s, C_t<T>* __restrict__ dst, const C_t<T>* __restrict__ tw1,
+                                             unsigned char* smem_raw) {
+  using C = C_t<T>;
+  using PL = ColPlan<N1, T>;
+  constexpr int E = PL::E, SLOTS = 2 * PL::X, TT = N1 / E;
+  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
+  const int col = s * SLOTS + slot;
+  C v[E];
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) {
+      const int k1 = j + b * TT + i * (N1 / R0);
+      const int r = k1 / n1_per, k1l = k1 - r * n1_per;
+      v[b * R0 + i] = __ldcs(&src[(((int64_t)r * n0_per + j0l) * n1_per + k1l) * m + col]);
+    }
+  ColEx<C, SLOTS> ex{reinterpret_cast<C*>(smem_raw), slot};
+  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+    for (int i = 0; i < RL; ++i) __stcg(&dst[(int64_t)(j + b * TT + i * (N1 / RL)) * m + col], v[b * RL + i]);
+}
+
+template <int N1, int M, typename T>
+constexpr int rows3_per_tile() {
+  return rows_per_tile<N1, M, T>();
+}
+
+// Pass B: persistent over this rank's planes (same ticket/ring scheme as
+// k_fused2d: C(p) tiles = axis-1 strips, R(p) tiles = rows).
+template <typename T, int N1, int M>
+__global__ void __launch_bounds__(col_threads<N1, T>())
+    k_3d_planes(F2Sched q, const C_t<T>* __restrict__ src, int n0_per, int n1_per, C_t<T>* __restrict__ ring,
+                T* __restrict__ out, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_ticket;
+  constexpr int RPT = rows_per_tile<N1, M, T>();
+  const uint64_t slot_elems = (uint64_t)N1 * M;
+  const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
+  const uint32_t total = q.F * G;
+  uint32_t next_ticket = 0;
+  if (threadIdx.x == 0) next_ticket = atomicAdd(q.ticket, 1u);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_ticket = next_ticket;
+      if (next_ticket < total) next_ticket = atomicAdd(q.ticket, 1u);
+    }
+    __syncthreads();
+    uint32_t t = s_ticket;
+    if (t >= total) break;
+    bool col;
+    uint32_t f, idx;
+    if (t < pro) {
+      col = true;
+      f = t / q.strips;
+      idx = t % q.strips;
+    } else if ((t -= pro) < nfull * G) {
+      const uint32_t g = t / G, r = t % G;
+      col = r < q.strips;
+      f = col ? g + q.L : g;
+      idx = col ? r : r - q.strips;
+    } else {
+      t -= nfull * G;
+      col = false;
+      f = nfull + t / q.rtiles;
+      idx = t % q.rtiles;
+    }
+    const uint32_t slot = f % q.S, use = f / q.S;
+    C_t<T>* Wp = ring + slot * slot_elems;
+    if (col) {
+      wait_geq(&q.row_done[slot], use * q.rtiles);
+      c2c_col_tile<T, N1>(src, (int)f, n0_per, n1_per, M, (int)idx, Wp, tw1, smem_raw);
+      signal_done(&q.col_done[slot]);
+    } else {
+      wait_geq(&q.col_done[slot], (use + 1) * q.strips);
+      row_tile<T, M, RPT>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw);
+      signal_done(&q.row_done[slot]);
+    }
+  }
+}
+
+template <int N1, int M, typename T>
+constexpr size_t planes_smem() {
+  using C = C_t<T>;
+  constexpr size_t a = (size_t)N1 * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
+  return a > b ? a : b;
+}
+
+}  // namespace grfc

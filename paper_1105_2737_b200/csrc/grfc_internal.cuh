@@ -314,6 +314,73 @@ __device__ __forceinline__ T sqrt_gamma(const GridDesc& g, const DensityDesc& D,
   return (T)0;
 }
 
+// ---------------------------------------------------------------- cell rules
+__device__ __forceinline__ void decode_half(const GridDesc& g, int64_t h, int64_t* k) {
+  k[g.d - 1] = h % g.hd;
+  int64_t r = h / g.hd;
+  for (int a = g.d - 2; a >= 0; --a) {
+    k[a] = r % g.n[a];
+    r /= g.n[a];
+  }
+}
+
+__device__ __forceinline__ void wrap_freq(const GridDesc& g, const int64_t* k, int64_t* kw) {
+  for (int a = 0; a < g.d; ++a) kw[a] = (k[a] <= g.n[a] / 2) ? k[a] : k[a] - g.n[a];
+}
+
+// Unit-variance Hermitian noise w(K) for a half-lattice cell with the device
+// Philox stream — the closed forms of SURVEY.md §A.3, verified against
+// src/hermitian.cpp:128-203:
+//  overwrite (Alg 2): counter = row-major H index c; self-conjugate -> a_c;
+//    otherwise, if the mirror -K lies in H (k_d in {0, N_d/2}) and is visited
+//    later (c(-K) > c), the later visit's draws win: r (a_{c(-K)} - i b_{c(-K)});
+//    else r (a_c + i b_c).
+//  exact set (Alg 3): counter = full-lattice index of rep(K), rep(K) = K iff
+//    K is self-conjugate or its lowest non-{0,N/2} component is < N/2
+//    (hermitian.cpp:39-84 membership); conjugated when K != rep(K).
+template <typename T>
+__device__ __forceinline__ C_t<T> philox_cell_noise(const GridDesc& g, int alg, const int64_t* k, int64_t h,
+                                                    const PhiloxKey& key, uint64_t field) {
+  using C = C_t<T>;
+  const T r = (T)0.70710678118654752440;
+  bool self = true;
+  for (int a = 0; a < g.d; ++a)
+    if (k[a] != 0 && k[a] != g.n[a] / 2) self = false;
+  uint64_t u, Uh;
+  bool conj = false;
+  if (alg == GRFC_ONE_FFT_OVERWRITE) {
+    Uh = ((uint64_t)g.cells + 1) / 2;
+    u = (uint64_t)h;
+    const int64_t kd = k[g.d - 1];
+    if (!self && (kd == 0 || kd == g.n[g.d - 1] / 2)) {
+      int64_t hm = 0;
+      for (int a = 0; a < g.d - 1; ++a) hm = hm * g.n[a] + (k[a] == 0 ? 0 : g.n[a] - k[a]);
+      hm = hm * g.hd + kd;
+      if (hm > h) {
+        u = (uint64_t)hm;
+        conj = true;
+      }
+    }
+  } else {  // exact set
+    Uh = ((uint64_t)g.points + 1) / 2;
+    bool is_rep = true;
+    if (!self)
+      for (int a = 0; a < g.d; ++a)
+        if (k[a] != 0 && k[a] != g.n[a] / 2) {
+          is_rep = k[a] < g.n[a] / 2;
+          break;
+        }
+    int64_t lin = 0;
+    for (int a = 0; a < g.d; ++a) lin = lin * g.n[a] + (is_rep ? k[a] : (k[a] == 0 ? 0 : g.n[a] - k[a]));
+    u = (uint64_t)lin;
+    conj = !is_rep;
+  }
+  T z0, z1;
+  unit_pair<T>(key, field, u, Uh, z0, z1);
+  if (self) return mk<C>(z0, (T)0);
+  return mk<C>(r * z0, conj ? -r * z1 : r * z1);
+}
+
 // ---------------------------------------------------------------- launch accounting
 void count_launch(uint64_t n = 1);
 

@@ -112,6 +112,9 @@ def _load():
         "grfc_generate_injected_host": [P, P, C.c_uint64, P],
         "grfc_dft_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_conjugate_reps": [C.c_int, P, P, P, C.c_uint64, P],
+        "grfc_slab_sizes": [P, C.c_int, P, P, P],
+        "grfc_slab_pass_a": [P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, P, P],
+        "grfc_slab_pass_b": [P, C.c_int, P, P, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -132,7 +135,8 @@ EXPORTED = (
     "grfc_plan_set_sqrt_gamma_table", "grfc_plan_destroy", "grfc_generate", "grfc_generate_host",
     "grfc_generate_injected", "grfc_half_noise_from_draws", "grfc_dump_noise", "grfc_dft_c2c", "grfc_plan_info",
     "grfc_last_launch_count", "grfc_kernel_timing_enable", "grfc_kernel_timing_read",
-    "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps",
+    "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps", "grfc_slab_sizes",
+    "grfc_slab_pass_a", "grfc_slab_pass_b",
 )
 
 
@@ -279,6 +283,19 @@ class Plan:
         out = np.zeros(n, np.float64)
         _check(_lib.grfc_dump_noise(self._h, seed, field, out.ctypes.data_as(C.c_void_p), n))
         return out
+
+    # ---- slab decomposition of one 3D field (include/grfc.h grfc_slab_*)
+    def slab_sizes(self, world: int):
+        """(buffer complex elements, block complex elements, slab points) per rank."""
+        b, k, s = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        _check(_lib.grfc_slab_sizes(self._h, world, C.byref(b), C.byref(k), C.byref(s)))
+        return int(b.value), int(k.value), int(s.value)
+
+    def slab_pass_a(self, world: int, rank: int, seed: int, field: int, d_send: int, stream: int = 0):
+        _check(_lib.grfc_slab_pass_a(self._h, world, rank, seed, field, C.c_void_p(d_send), C.c_void_p(stream)))
+
+    def slab_pass_b(self, world: int, d_recv: int, d_out: int, stream: int = 0):
+        _check(_lib.grfc_slab_pass_b(self._h, world, C.c_void_p(d_recv), C.c_void_p(d_out), C.c_void_p(stream)))
 
     # ---- torch conveniences (torch is plumbing: device memory and streams)
     def generate_tensor(self, seed: int, first_field: int = 0, nfields: int = 1, out=None, stream=None):
