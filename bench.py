@@ -366,11 +366,95 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_slab(args, cfg):
+    """c4 on N > 1 GPUs: ONE 512^3 field slab-decomposed over the ranks
+    (strong scaling). Per step: pass A (generation + axis-0 FFT of the rank's
+    spectrum slab) -> NCCL all_to_all_single of contiguous blocks over NVLink
+    -> pass B (axis-1/2 FFTs of the rank's field planes). include/grfc.h
+    grfc_slab_*."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1105_2737_b200 import grfc
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    counts = cfg["counts"]
+    d = len(counts)
+    dens = grfc.Density.gaussian_cov(d, cfg["density"][1])
+    plan = grfc.Plan(counts, (1.0,) * d, dens, grfc.ONE_FFT_OVERWRITE, grfc.F32, device=local)
+    buf, block, slab_pts = plan.slab_sizes(world)
+    send = torch.empty(2 * buf, dtype=torch.float32, device="cuda")  # complex64 as float pairs
+    recv = torch.empty_like(send)
+    out = torch.empty(slab_pts, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(field):
+        plan.slab_pass_a(world, rank, 0, field, send.data_ptr(), stream.cuda_stream)
+        dist.all_to_all_single(recv, send)
+        plan.slab_pass_b(world, recv.data_ptr(), out.data_ptr(), stream.cuda_stream)
+
+    for i in range(args.warmup):
+        step(i)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        end.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([start.elapsed_time(end) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    P = 1
+    for n in counts:
+        P *= n
+    value = P / (ms / 1e3) / 1e9
+    # end to end: the rank's slab copied to pinned host memory every step
+    host = torch.empty(slab_pts, dtype=torch.float32, pin_memory=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(max(2, min(args.steps, 5))):
+        step(i)
+        host.copy_(out, non_blocking=False)
+    e2e_ms = (time.perf_counter() - t0) / max(2, min(args.steps, 5)) * 1e3
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    peak, kind = hbm_peak()
+    if rank == 0:
+        nvl = 2 * buf * 4 * (world - 1) / world  # bytes each rank sends over NVLink per step
+        line = {
+            "metric": "GRF grid points/sec (Gpts/s)", "value": value, "unit": "Gpts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "config": args.config, "counts": list(counts),
+                       "parallelism": f"slab x{world} (NCCL all_to_all_single between pass A and pass B)",
+                       "path": plan.path, "l2": "output 512 MiB per step > L2"},
+            "path_roofline": {"bound": "hbm", "achieved": P * 4 / (ms / 1e3) / 1e9 / world, "peak": peak,
+                              "unit": "GB/s per GPU", "frac": P * 4 / (ms / 1e3) / 1e9 / world / peak},
+            "nvlink_bytes_per_rank_per_step": nvl,
+            "e2e": {"value": P / (float(te.item()) / 1e3) / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": P * 4, "ms_per_step": float(te.item())},
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+    elif args.config == "c4" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_slab(args, cfg)
     else:
         run_ours(args, cfg)
 
