@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="c4: force the slab (multi-GPU) leg, also at N=1")
     return ap.parse_args()
 
 
@@ -377,8 +378,12 @@ def run_slab(args, cfg):
 
     from paper_1105_2737_b200 import grfc
 
-    world = int(os.environ["WORLD_SIZE"])
-    rank = int(os.environ["RANK"])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    os.environ.setdefault("RANK", str(rank))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -453,7 +458,7 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
-    elif args.config == "c4" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    elif args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.slab):
         run_slab(args, cfg)
     else:
         run_ours(args, cfg)

@@ -1,0 +1,289 @@
+// Fused power-of-two 2D path for Algorithm 1 (two-FFT, the reference's
+// synth.cpp:81-116): white noise -> exp(+) transform -> x sqrt(g) sqrt((2pi)^d P/|A|)
+// -> exp(-) transform / P -> real part.
+//
+// Tiles (persistent, one launch per batch, per-field ring slot in L2):
+//   R1  rows: noise z(j1, m) = (x(j1, 2m), x(j1, 2m+1)) from Philox units
+//       u = j1 M + m (rows j1 and j1 + N1/2 share one call), exp(+) M-point
+//       row FFT -> Zf(j1, k) into the slot.
+//   C   column pair (k, M-k): R2C split (X = (Zf_k + conj Zf_{M-k})/2
+//       - i e^{2pi i k/N2} (Zf_k - conj Zf_{M-k})/2; k = 0 packs DC + i Nyquist),
+//       exp(+) column FFT, x sqrt(g)*scale (packed column unpacked through its
+//       mirror row), then the C2R pre-twiddle of the exp(-) inverse written as
+//       an exp(+) transform of conj(V):
+//         Zh(k1,k) = (conj V(k1,k) + V(-k1,M-k)) + i e^{2pi i k/N2} (conj V(k1,k) - V(-k1,M-k)),
+//       exp(+) column FFT -> Z(j1, k) in place.
+//   R2  rows: row_tile (M-point exp(+) FFT -> the field rows), as Algorithm 2.
+#pragma once
+
+#include "fast2d_kernels.cuh"
+
+namespace grfc {
+
+struct F2Sched3 {
+  uint32_t* ticket;
+  uint32_t* r1_done;   // [S]
+  uint32_t* col_done;  // [S]
+  uint32_t* row_done;  // [S]
+  uint32_t F, L, S, g1, gc, g2;
+};
+
+template <typename T>
+__device__ __forceinline__ C_t<T> half_c(C_t<T> a) {
+  return mk<C_t<T>>(a.x * (T)0.5, a.y * (T)0.5);
+}
+
+// R1: rows r0 + p and r0 + p + N1/2 for p < RPT/2 (Philox pair sharing).
+template <typename T, int N1, int M, int RPT>
+__device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int r0,
+                                        C_t<T>* __restrict__ Wf, const C_t<T>* __restrict__ tw2,
+                                        unsigned char* smem_raw) {
+  using C = C_t<T>;
+  using PL = RowPlan<M, T>;
+  constexpr int E = PL::E, TT = M / E, H = RPT / 2, PITCH = row_pitch<M, C>();
+  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  const uint64_t uh = (uint64_t)(N1 / 2) * M;
+  for (int it = threadIdx.x; it < H * M; it += blockDim.x) {
+    const int pr = it / M, m = it - pr * M;
+    const uint64_t u = (uint64_t)(r0 + pr) * M + m;
+    T a0, b0, a1, b1;
+    if constexpr (sizeof(T) == 4) {
+      unit_quad_f32(key, fld, u, a0, b0, a1, b1);
+    } else {
+      unit_pair<T>(key, fld, u, uh, a0, b0);
+      unit_pair<T>(key, fld, u + uh, uh, a1, b1);
+    }
+    sm[pr * PITCH + RowEx<C>::pad(m)] = mk<C>(a0, b0);
+    sm[(pr + H) * PITCH + RowEx<C>::pad(m)] = mk<C>(a1, b1);
+  }
+  __syncthreads();
+  const int tid = threadIdx.x, rl = tid / TT, j = tid % TT;
+  const bool live = rl < RPT;
+  const int rs = live ? rl : 0;
+  C v[E];
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[rs * PITCH + RowEx<C>::pad(j + b * TT + i * (M / R0))];
+  __syncthreads();
+  RowEx<C> ex{sm + rs * PITCH, live};
+  line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
+  if (!live) return;
+  const int row = rl < H ? r0 + rl : r0 + (rl - H) + N1 / 2;
+  C* o = Wf + (int64_t)row * M;
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+    for (int i = 0; i < RL; ++i) __stcg(&o[j + b * TT + i * (M / RL)], v[b * RL + i]);
+}
+
+// C: forward column FFT, spectral scaling, inverse pre-twiddle, column FFT.
+template <typename T, int N1>
+__device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
+                                              const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
+                                              unsigned char* smem_raw) {
+  using C = C_t<T>;
+  using PL = ColPlan<N1, T>;
+  constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
+  constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS, pslot = slot ^ CB;
+  bool packed, mid;
+  const int col = slot_column(s, slot, CB, p.m, packed, mid);
+  const int pcol = p.m - col;  // Zh partner column (for packed: M)
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  const T half = (T)0.5;
+  // 1. Zf columns -> smem [j1][slot]
+#pragma unroll 4
+  for (int t = 0; t < E; ++t) {
+    const int j1 = j + t * TT;
+    sm[j1 * SLOTS + slot] = __ldcg(&Wf[(int64_t)j1 * p.m + col]);
+  }
+  __syncthreads();
+  // 2. R2C split into the stage-0 registers
+  const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
+  C v[E];
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) {
+      const int j1 = j + b * TT + i * (N1 / R0);
+      const C A = sm[j1 * SLOTS + slot];
+      C X;
+      if (packed) {
+        X = mk<C>(A.x + A.y, A.x - A.y);  // X(j1,0) + i X(j1,M)
+      } else if (mid) {
+        X = A;
+      } else {
+        const C B = sm[j1 * SLOTS + pslot];
+        const C sum = mk<C>(A.x + B.x, A.y - B.y), dif = mk<C>(A.x - B.x, A.y + B.y);
+        const C t = cmul(w, dif);
+        X = mk<C>((sum.x + t.y) * half, (sum.y - t.x) * half);
+      }
+      v[b * R0 + i] = X;
+    }
+  __syncthreads();
+  ColEx<C, SLOTS> ex{sm, slot};
+  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+  // 3. U -> smem in natural row order
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+    for (int i = 0; i < RL; ++i) sm[(j + b * TT + i * (N1 / RL)) * SLOTS + slot] = v[b * RL + i];
+  __syncthreads();
+  // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col)
+  const T sc = (T)p.scale;
+#pragma unroll
+  for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+    for (int i = 0; i < R0; ++i) {
+      const int k1 = j + b * TT + i * (N1 / R0), km = (N1 - k1) & (N1 - 1);
+      C Vk, Vm;
+      if (packed) {
+        const C Uk = sm[k1 * SLOTS + slot], Um = sm[km * SLOTS + slot];
+        // F0(k1) = (U(k1) + conj U(-k1))/2 ; FM(-k1) = -i (U(-k1) - conj U(k1))/2
+        const C F0k = mk<C>((Uk.x + Um.x) * half, (Uk.y - Um.y) * half);
+        const C FMm = mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half);
+        Vk = cscale(F0k, sqrt_g2<T>(p, k1, 0) * sc);
+        Vm = cscale(FMm, sqrt_g2<T>(p, km, p.m) * sc);
+      } else {
+        Vk = cscale(sm[k1 * SLOTS + slot], sqrt_g2<T>(p, k1, col) * sc);
+        Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], sqrt_g2<T>(p, km, mid ? col : pcol) * sc);
+      }
+      const C cV = cconj(Vk);
+      const C sum = cadd(cV, Vm), dif = csub(cV, Vm);
+      const C t = cmul(w, dif);
+      v[b * R0 + i] = mk<C>(sum.x - t.y, sum.y + t.x);
+    }
+  __syncthreads();
+  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+    for (int i = 0; i < RL; ++i) __stcg(&Wf[(int64_t)(j + b * TT + i * (N1 / RL)) * p.m + col], v[b * RL + i]);
+}
+
+template <typename T, int N1, int M>
+__global__ void __launch_bounds__(fused_threads<N1, M, T>())
+    k_fused2d_alg1(F2Params p, F2Sched3 q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring,
+                   T* __restrict__ out, int64_t out_stride, const C_t<T>* __restrict__ tw1,
+                   const C_t<T>* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_ticket;
+  constexpr int RPT = rows_per_tile<N1, M, T>();
+  const uint64_t slot_elems = (uint64_t)N1 * M;
+  const uint32_t L = q.L, F = q.F, g1 = q.g1, gc = q.gc, g2 = q.g2;
+  // ticket ranges (L <= F/2): [0,L): R1 | [L,2L): R1 C | [2L,F): R1 C R2 | [F,F+L): C R2 | [F+L,F+2L): R2
+  const uint32_t nA = L * g1, nB = L * (g1 + gc), nC = (F - 2 * L) * (g1 + gc + g2), nD = L * (gc + g2);
+  const uint32_t total = F * (g1 + gc + g2);
+  uint32_t next_ticket = 0;
+  if (threadIdx.x == 0) next_ticket = atomicAdd(q.ticket, 1u);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_ticket = next_ticket;
+      if (next_ticket < total) next_ticket = atomicAdd(q.ticket, 1u);
+    }
+    __syncthreads();
+    uint32_t t = s_ticket;
+    if (t >= total) break;
+    int kind;  // 0 R1, 1 C, 2 R2
+    uint32_t f, idx;
+    if (t < nA) {
+      kind = 0, f = t / g1, idx = t % g1;
+    } else if ((t -= nA) < nB) {
+      const uint32_t g = t / (g1 + gc), r = t % (g1 + gc);
+      if (r < g1) kind = 0, f = L + g, idx = r;
+      else kind = 1, f = g, idx = r - g1;
+    } else if ((t -= nB) < nC) {
+      const uint32_t g = t / (g1 + gc + g2), r = t % (g1 + gc + g2);
+      if (r < g1) kind = 0, f = 2 * L + g, idx = r;
+      else if (r < g1 + gc) kind = 1, f = L + g, idx = r - g1;
+      else kind = 2, f = g, idx = r - g1 - gc;
+    } else if ((t -= nC) < nD) {
+      const uint32_t g = t / (gc + g2), r = t % (gc + g2);
+      if (r < gc) kind = 1, f = F - L + g, idx = r;
+      else kind = 2, f = F - 2 * L + g, idx = r - gc;
+    } else {
+      t -= nD;
+      kind = 2, f = F - L + t / g2, idx = t % g2;
+    }
+    const uint32_t slot = f % q.S, use = f / q.S;
+    C_t<T>* Wf = ring + slot * slot_elems;
+    if (kind == 0) {
+      wait_geq(&q.row_done[slot], use * g2);
+      r1_tile<T, N1, M, RPT>(p, key, field0 + f, (int)idx * (RPT / 2), Wf, tw2, smem_raw);
+      signal_done(&q.r1_done[slot]);
+    } else if (kind == 1) {
+      wait_geq(&q.r1_done[slot], (use + 1) * g1);
+      alg1_col_tile<T, N1>(p, (int)idx, Wf, tw1, tw2, smem_raw);
+      signal_done(&q.col_done[slot]);
+    } else {
+      wait_geq(&q.col_done[slot], (use + 1) * gc);
+      row_tile<T, M, RPT>(Wf, (int)idx * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw);
+      signal_done(&q.row_done[slot]);
+    }
+  }
+}
+
+inline size_t alg1_ctr_bytes(uint32_t S) { return ((1 + 3 * (size_t)S) * 4 + 255) / 256 * 256; }
+
+inline void alg1_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, uint32_t* L, uint32_t* S,
+                          uint32_t* conc) {
+  const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + 2 * rtiles);
+  uint32_t l = (3 * c + G - 1) / G;
+  l = l < 1 ? 1 : l;
+  l = l < (uint32_t)(nf / 2) ? l : (uint32_t)(nf / 2);
+  uint32_t s = 2 * l + 2 * ((c + G - 1) / G) + 2;
+  s = s < (uint32_t)nf ? s : (uint32_t)nf;
+  *L = l;
+  *S = s;
+  *conc = c;
+}
+
+template <typename T, int N1, int M>
+cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out, int64_t stride,
+                              cudaStream_t s) {
+  using C = C_t<T>;
+  constexpr int NT = fused_threads<N1, M, T>(), RPT = rows_per_tile<N1, M, T>();
+  constexpr size_t smem = fused_smem<N1, M, T>();
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_fused2d_alg1<T, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d_alg1<T, N1, M>, NT, smem);
+    if (occ < 1) occ = 1;
+  }
+  F2Sched3 q{};
+  uint32_t conc = 0;
+  alg1_geometry(f.sms, occ, M / (2 * ColPlan<N1, T>::X), N1 / RPT, nf, &q.L, &q.S, &conc);
+  q.F = (uint32_t)nf;
+  q.g1 = (uint32_t)(N1 / RPT);
+  q.gc = (uint32_t)(M / (2 * ColPlan<N1, T>::X));
+  q.g2 = (uint32_t)(N1 / RPT);
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, alg1_ctr_bytes(q.S) + (size_t)q.S * N1 * M * sizeof(C), s);
+  if (e != cudaSuccess) return e;
+  uint32_t* ctr = (uint32_t*)ws;
+  q.ticket = ctr;
+  q.r1_done = ctr + 1;
+  q.col_done = ctr + 1 + q.S;
+  q.row_done = ctr + 1 + 2 * q.S;
+  C* ring = (C*)((char*)ws + alg1_ctr_bytes(q.S));
+  e = cudaMemsetAsync(ctr, 0, (1 + 3 * q.S) * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const C* tw1 = (const C*)f.d_tw;
+  const C* tw2 = tw1 + f.n1;
+  F2Params p = make_params(f);
+  p.scale = f.s_two;
+  p.f_scale = (float)f.s_two;
+  const uint32_t total = q.F * (q.g1 + q.gc + q.g2);
+  const uint32_t grid = total < conc ? total : conc;
+  {
+    LaunchScope ls("fused2d_alg1_persistent", s);
+    k_fused2d_alg1<T, N1, M><<<grid, NT, smem, s>>>(p, q, philox_key(seed), field0, ring, (T*)out, stride, tw1, tw2);
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(ws, s);
+  return e;
+}
+
+}  // namespace grfc

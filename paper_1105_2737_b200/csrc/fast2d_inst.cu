@@ -2,7 +2,7 @@
 // length N1) pair; the Makefile compiles this file once per pair with
 // -DINST_T=<float|double> -DINST_N=<N1> so the objects build in parallel.
 // Rows are instantiated for M = N1/2 (covers every supported N2 = 2M).
-#include "fast2d_kernels.cuh"
+#include "fast2d_alg1.cuh"
 
 namespace grfc {
 template cudaError_t launch_cols<INST_T, INST_N, GRFC_ONE_FFT_OVERWRITE>(const Fast2D&, uint64_t, uint64_t, int64_t,
@@ -14,13 +14,13 @@ template cudaError_t launch_rows<INST_T, INST_N / 2>(const Fast2D&, int64_t, con
 #define GRFC_FUSED(M)                                                                                    \
   template cudaError_t launch_fused<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(                                \
       const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*, int64_t, cudaStream_t);                        \
-  template cudaError_t launch_fused<INST_T, INST_N, M, GRFC_ONE_FFT_RECURSIVE>(                                \
-      const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*, int64_t, cudaStream_t);                        \
-  template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(Fast2D&);                        \
-  template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_RECURSIVE>(Fast2D&);
+  template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(Fast2D&);
 GRFC_FUSED(128)
 GRFC_FUSED(256)
 GRFC_FUSED(512)
 GRFC_FUSED(1024)
 GRFC_FUSED(2048)
+// Algorithm 1 (three-tile persistent kernel): square grids, M = N1/2.
+template cudaError_t launch_fused_alg1<INST_T, INST_N, INST_N / 2>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,
+                                                                  int64_t, cudaStream_t);
 }  // namespace grfc

@@ -21,14 +21,18 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
                          int64_t stride, cudaStream_t s);
 template <typename T, int N1, int M, int ALG>
 cudaError_t fused_query(Fast2D& f);
+template <typename T, int N1, int M>
+cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out, int64_t stride,
+                              cudaStream_t s);
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 
 bool fast2d_supported(int d, const int64_t* n, int dtype, int alg, int family) {
   (void)dtype;
   (void)family;
-  if (d != 2 || alg == GRFC_TWO_FFT) return false;
+  if (d != 2) return false;
   if (!is_pow2(n[0]) || !is_pow2(n[1])) return false;
+  if (alg == GRFC_TWO_FFT && n[0] != n[1]) return false;  // fused Algorithm 1: square grids
   return n[0] >= 256 && n[0] <= 4096 && n[1] >= 256 && n[1] <= 4096;
 }
 
@@ -94,6 +98,21 @@ static cudaError_t dispatch_rows(const Fast2D& f, int64_t nf, const void* W, voi
 
 #define GRFC_CALL_FUSED(T, N1, M, ALG) launch_fused<T, N1, M, ALG>(f, seed, field0, nf, W, out, stride, s)
 #define GRFC_CALL_QUERY(T, N1, M, ALG) fused_query<T, N1, M, ALG>(f)
+#define GRFC_CALL_ALG1(T, N1, M, ALG) launch_fused_alg1<T, N1, M>(f, seed, field0, nf, out, stride, s)
+
+template <typename T>
+static cudaError_t dispatch_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out,
+                                 int64_t stride, cudaStream_t s) {
+  if (f.n2 != f.n1) return cudaErrorNotSupported;
+  switch (f.n1) {
+    case 256: return GRFC_CALL_ALG1(T, 256, 128, 0);
+    case 512: return GRFC_CALL_ALG1(T, 512, 256, 0);
+    case 1024: return GRFC_CALL_ALG1(T, 1024, 512, 0);
+    case 2048: return GRFC_CALL_ALG1(T, 2048, 1024, 0);
+    case 4096: return GRFC_CALL_ALG1(T, 4096, 2048, 0);
+  }
+  return cudaErrorNotSupported;
+}
 
 template <typename T, int ALG>
 static cudaError_t dispatch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
@@ -109,10 +128,8 @@ static cudaError_t dispatch_query(Fast2D& f) {
 template <typename T>
 static cudaError_t run_fast(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                             int64_t stride, cudaStream_t s) {
-  if (f.persistent)
-    return alg == GRFC_ONE_FFT_OVERWRITE
-               ? dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s)
-               : dispatch_fused<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, out, stride, s);
+  if (f.persistent && alg == GRFC_ONE_FFT_OVERWRITE)
+    return dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s);
   cudaError_t e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_cols<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, s)
                                                 : dispatch_cols<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, s);
   if (e != cudaSuccess) return e;
@@ -163,14 +180,12 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   // two-stream column/row kernel pipeline (A/B testing).
   const char* pe = std::getenv("GRFC_PERSISTENT");
   f.persistent = !(pe && pe[0] == '0');
+  // Persistent fused kernel: Algorithm 2; Algorithm 3 uses the column/row kernel pair.
+  if (alg != GRFC_ONE_FFT_OVERWRITE) f.persistent = false;
   if (!f.persistent) return cudaSuccess;
   f.fail_what = "persistent kernel query";
-  if (dtype == GRFC_F64)
-    e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
-                                      : dispatch_query<double, GRFC_ONE_FFT_RECURSIVE>(f);
-  else
-    e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f)
-                                      : dispatch_query<float, GRFC_ONE_FFT_RECURSIVE>(f);
+  e = dtype == GRFC_F64 ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
+                        : dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f);
   return e;
 }
 
@@ -209,6 +224,9 @@ cudaError_t fast2d_generate(Fast2D& f, int alg, uint64_t seed, uint64_t field0, 
                             int64_t stride, cudaStream_t s) {
   const size_t esz = f.dtype == GRFC_F64 ? 8 : 4;
   void* ws = nullptr;
+  if (alg == GRFC_TWO_FFT)  // Algorithm 1: always the persistent three-tile kernel
+    return f.dtype == GRFC_F64 ? dispatch_alg1<double>(f, seed, field0, nf, out, stride, s)
+                               : dispatch_alg1<float>(f, seed, field0, nf, out, stride, s);
   if (f.persistent) {
     cudaError_t e = cudaMallocAsync(&ws, fast2d_workspace_bytes(f, nf), s);
     if (e != cudaSuccess) return e;
