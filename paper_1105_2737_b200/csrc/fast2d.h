@@ -22,6 +22,7 @@ struct Fast2D {
   int kind = 0;
   // persistent fused kernel geometry (fused_query)
   bool persistent = false;
+  bool warp = false;  // warp-synchronous column tiles + transposed W (fast2d_warp.cuh)
   int occ = 1, sms = 148, strips = 0, rtiles = 0;
   // two-stream pipeline: column kernels on sa, row kernels on sb, a ring of
   // kRing chunk slots ordered by events (no in-kernel waiting).

@@ -175,6 +175,19 @@ __device__ __forceinline__ void run_stages(C* v, int j, const C* __restrict__ tw
   }
 }
 
+template <typename RS>
+struct RNext;
+template <int R0, int R1, int... Rs>
+struct RNext<Radices<R0, R1, Rs...>> {
+  static constexpr int value = R1;
+};
+
+// Stages 1.. of a plan (stage 0 already applied, v holding stage-1 inputs).
+template <int N, int E, int SIGN, int NS, typename C, typename Ex, int R0, int... Rs>
+__device__ __forceinline__ void run_rest(C* v, int j, const C* __restrict__ tw, int tws, Ex& ex, Radices<R0, Rs...>) {
+  run_stages<N, E, SIGN, NS, Rs...>(v, j, tw, tws, ex);
+}
+
 template <int N, int E, int SIGN, typename C, typename Ex, int... Rs>
 __device__ __forceinline__ void line_fft(C* v, int j, const C* __restrict__ tw, int tws, Ex& ex,
                                          Radices<Rs...>) {

@@ -49,7 +49,8 @@ def main(rep, obj, kname, top=40):
     for fn in os.listdir(srcdir):
         src[fn] = open(os.path.join(srcdir, fn)).read().split("\n")
     print(f"total warp-instr {te}  stall samples {ts}")
-    for k in sorted(ex, key=lambda k: -ex[k])[:top]:
+    key = st if os.environ.get("SORT") == "stall" else ex
+    for k in sorted(key, key=lambda k: -key[k])[:top]:
         fn, ln = k
         txt = src[fn][ln - 1].strip()[:84] if fn in src and ln > 0 else ""
         print(f"{fn:20s}:{ln:<5d} ex {100 * ex[k] / te:5.1f}%  st {100 * st[k] / ts:5.1f}%  {txt}")
