@@ -156,15 +156,28 @@ def cpu_reference_rate(cfg, alg, nfields, threads):
     return pts / secs / 1e9, kind, threads, secs
 
 
+def sized_sample(cfg, alg, threads, target_s):
+    """Fields per sample so one sample takes ~target_s wall on `threads` threads
+    (probe: one field per thread; 512^3 is a single field)."""
+    import math
+
+    if math.prod(cfg["counts"]) > 2 ** 26:
+        return 1
+    probe = max(1, threads)
+    _, _, _, secs = cpu_reference_rate(cfg, alg, probe, threads)
+    n = int(probe * target_s / max(secs, 1e-3))
+    n = max(probe, (n // probe) * probe)
+    return min(n, 256 * probe)
+
+
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     alg = cfg["algs"][0]
-    nfields = max(8, 4 * threads) if cfg["counts"] != (512, 512, 512) else 1
-    if cfg["counts"] == (4096, 4096):
-        nfields = max(2, threads)
+    # each step: a bounded sample of ~1 s wall on all host threads (the whole run stays within minutes)
+    nfields = sized_sample(cfg, alg, threads, target_s=1.0)
     for _ in range(max(0, args.warmup)):
         cpu_reference_rate(cfg, alg, max(1, nfields // 4), threads)
     rates, secs_all = [], 0.0
@@ -333,10 +346,8 @@ def run_ours(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        nf = max(8, 4 * threads) if P <= 2 ** 22 else max(2, threads // 2)
-        if P > 2 ** 26:
-            nf = 1
         try:
+            nf = sized_sample(cfg, main_alg, threads, target_s=10.0)  # ~10 s of host work
             rate, kind, used, secs = cpu_reference_rate(cfg, main_alg, nf, threads)
             cpu = {"value": rate, "unit": "Gpts/s", "cores": used, "kind": kind,
                    "sample": f"{nf} fields of this workload (Algorithm {main_alg + 1 if main_alg else 1}, fp64) "

@@ -23,13 +23,14 @@ KEYS = [
 def main(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
+    unit = dict(zip(hdr, units))
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         print("==", d.get("Kernel Name", "")[:100])
         for k in KEYS:
             if k in d:
-                print(f"  {k:70s} {d[k]}")
+                print(f"  {k:70s} {d[k]} {unit.get(k, '')}")
         stalls = {k: d[k] for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
         tot = sum(float(v or 0) for v in stalls.values())
         for k, v in sorted(stalls.items(), key=lambda kv: -float(kv[1] or 0))[:8]:

@@ -13,7 +13,7 @@ from bench import CONFIGS  # noqa: E402
 from paper_1105_2737_b200 import grfc  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-nf = int(sys.argv[2]) if len(sys.argv) > 2 else cfg["fields"]
+nf = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else cfg["fields"]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 alg = int(os.environ.get("GRFC_ALG", cfg["algs"][0]))
 d = len(cfg["counts"])
