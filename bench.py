@@ -167,7 +167,7 @@ def sized_sample(cfg, alg, threads, target_s):
     _, _, _, secs = cpu_reference_rate(cfg, alg, probe, threads)
     n = int(probe * target_s / max(secs, 1e-3))
     n = max(probe, (n // probe) * probe)
-    return min(n, 256 * probe)
+    return min(n, 2048 * probe)
 
 
 def run_reference_arm(args, cfg):
