@@ -187,6 +187,43 @@ grfc_status grfc_slab_pass_a(grfc_plan plan, int world, int rank, uint64_t seed,
                              void* stream);
 grfc_status grfc_slab_pass_b(grfc_plan plan, int world, const void* d_recv, void* d_out, void* stream);
 
+/* Monte-Carlo covariance against one reference grid point — the device form
+ * of grf::estimate_covariance (src/stats.cpp:39-97, include/grf/stats.hpp):
+ *   est[K] = M^-1 sum_{j<M} f_j[ref] f_j[K],   f_j = field (seed, j) of grfc_generate
+ * (the reference's substream (seed, j), stats.cpp:105). Determinism as the
+ * reference (stats.cpp:17-18,60-93): samples in fixed chunks of
+ * GRFC_COV_CHUNK; per chunk and point, fp64 multiply-then-add in ascending j;
+ * chunk partials merged in chunk order with Kahan compensation; then x (1/M).
+ * Bit-identical for any generation batch size and any number of devices.
+ * `ref` is the row-major linear index of the reference point
+ * (GridSpec::linear_index). Errors: samples == 0 or ref out of range ->
+ * GRFC_EINVAL with the reference's messages (stats.cpp:43-45). Output: P
+ * doubles. */
+#define GRFC_COV_CHUNK 1024
+grfc_status grfc_estimate_covariance(grfc_plan plan, uint64_t seed, uint64_t samples, int64_t ref, double* d_out,
+                                     void* stream);
+/* Same, HOST output; synchronous (what the C++ drop-in calls). */
+grfc_status grfc_estimate_covariance_host(grfc_plan plan, uint64_t seed, uint64_t samples, int64_t ref,
+                                          double* h_out);
+/* Multi-device form: the partial sums of chunks [chunk0, chunk0+nchunks) of a
+ * `samples`-sample estimate (nchunks*P doubles, chunk-major) ... */
+grfc_status grfc_covariance_partials(grfc_plan plan, uint64_t seed, uint64_t samples, uint64_t chunk0,
+                                     uint64_t nchunks, int64_t ref, double* d_partials, void* stream);
+/* ... and their chunk-ordered Kahan merge scaled by 1/samples (all chunks, in
+ * order, gathered on one device): equals grfc_estimate_covariance bit for bit. */
+grfc_status grfc_covariance_merge(grfc_plan plan, const double* d_partials, uint64_t nchunks, uint64_t samples,
+                                  double* d_out, void* stream);
+/* Building block for caller-made fields (device, plan dtype, field j at
+ * d_fields + j*field_stride): d_acc[K] += sum_j f_j[ref] f_j[K], ascending j. */
+grfc_status grfc_covariance_accumulate(grfc_plan plan, const void* d_fields, uint64_t nfields,
+                                       uint64_t field_stride, int64_t ref, double* d_acc, void* stream);
+/* One chunk of the StreamFactory overload (stats.cpp:39-82): sample i is
+ * synthesized from draws + i*ndraws (reference draw order, as
+ * grfc_generate_injected); h_partial (P doubles, host) receives the chunk's
+ * partial sum. The caller merges chunks in order (Kahan) and scales by 1/M. */
+grfc_status grfc_covariance_chunk_injected_host(grfc_plan plan, const double* draws, uint64_t nsamples,
+                                                uint64_t ndraws, int64_t ref, double* h_partial);
+
 /* Plan introspection for benchmarks: bytes of workspace per field and the
  * kernel path chosen ("pow2-2d", "generic", ...). */
 grfc_status grfc_plan_info(grfc_plan plan, uint64_t* cells_half, uint64_t* points,

@@ -214,5 +214,24 @@ class Reference(_Lib):
         return secs.value, chk.value
 
 
+    def estimate_covariance_fixed(self, counts, lengths, dens, alg, reference, draws, threads=0):
+        """grf::estimate_covariance with per-sample FixedStreams: draws is (samples, ndraws)."""
+        draws = np.ascontiguousarray(draws, np.float64)
+        out = np.zeros(int(np.prod(counts)))
+        self._check(self.lib.ref_estimate_covariance_fixed(
+            len(counts), _i64(counts), _f64(lengths), C.byref(dens), alg, C.c_uint64(draws.shape[0]),
+            _i64(reference), _ptr(draws), C.c_uint64(draws.shape[1]), threads, _ptr(out)))
+        return out.reshape(counts)
+
+    def convergence_study(self, level_min, level_max, samples, alg, seed, threads=0):
+        rows = np.zeros(4 * 16)
+        n = C.c_int(0)
+        slope = C.c_double(0)
+        self._check(self.lib.ref_convergence_study(level_min, level_max, C.c_uint64(samples), alg,
+                                                   C.c_uint64(seed), threads, _ptr(rows), C.byref(n),
+                                                   C.byref(slope)))
+        return rows[:4 * n.value].reshape(n.value, 4), slope.value
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_LIB)

@@ -28,6 +28,7 @@
 #include "grf/dft.hpp"
 #include "grf/hermitian.hpp"
 #include "grf/spectral.hpp"
+#include "grf/stats.hpp"
 #include "grf/synth.hpp"
 
 namespace {
@@ -271,6 +272,43 @@ int ref_bench_batch(int dim, const int64_t* counts, const double* lengths, const
     double s = 0.0;
     for (double v : sums) s += v;
     if (checksum) *checksum = s;
+  });
+}
+
+// grf::estimate_covariance through the reference's StreamFactory overload
+// (stats.cpp:39-97): sample j replays draws[j*ndraws ...] through a
+// FixedStream. `ref` is the multi-index of the reference point.
+int ref_estimate_covariance_fixed(int dim, const int64_t* counts, const double* lengths, const ref_density* d,
+                                  int alg, uint64_t samples, const int64_t* ref, const double* draws,
+                                  uint64_t ndraws, int threads, double* out) {
+  return guarded([&] {
+    const grf::GridSpec grid = make_grid(dim, counts, lengths);
+    auto dens = make_density(d);
+    const grf::StreamFactory streams = [&](std::uint64_t j) {
+      return std::make_unique<grf::FixedStream>(
+          std::vector<double>(draws + j * ndraws, draws + (j + 1) * ndraws));
+    };
+    const grf::CovarianceEstimate e = grf::estimate_covariance(
+        grid, *dens, to_alg(alg), samples, grf::MultiIndex(ref, ref + dim), streams, threads);
+    std::memcpy(out, e.estimates.data(), sizeof(double) * e.estimates.size());
+  });
+}
+
+// grf::convergence_study (stats.cpp:141-174): rows (level, cells, max_err,
+// mc_floor) into rows[4*i..]; *nrows rows; *slope = fitted slope or NaN.
+int ref_convergence_study(int level_min, int level_max, uint64_t samples, int alg, uint64_t seed, int threads,
+                          double* rows, int* nrows, double* slope) {
+  return guarded([&] {
+    const grf::ConvergenceReport r =
+        grf::convergence_study(level_min, level_max, samples, to_alg(alg), seed, threads);
+    *nrows = static_cast<int>(r.rows.size());
+    for (std::size_t i = 0; i < r.rows.size(); ++i) {
+      rows[4 * i] = r.rows[i].level;
+      rows[4 * i + 1] = static_cast<double>(r.rows[i].cells);
+      rows[4 * i + 2] = r.rows[i].max_err;
+      rows[4 * i + 3] = r.rows[i].mc_floor;
+    }
+    *slope = r.fitted_slope ? *r.fitted_slope : std::nan("");
   });
 }
 

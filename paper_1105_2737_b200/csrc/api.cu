@@ -748,4 +748,187 @@ grfc_status grfc_slab_pass_b(grfc_plan p, int world, const void* d_recv, void* d
   return GRFC_OK;
 }
 
+// ---- Monte-Carlo covariance (stats.cu; reference src/stats.cpp:39-97) --------------------
+
+static grfc_status cov_check(grfc_plan p, uint64_t samples, int64_t ref) {
+  if (!p) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (samples < 1) return fail(GRFC_EINVAL, "estimate_covariance: need at least one sample");
+  if (ref < 0 || (uint64_t)ref >= p->points)
+    return fail(GRFC_EINVAL, "estimate_covariance: reference index out of range");
+  if (p->dens.family == GRFC_DENSITY_TABLE && !p->table_set)
+    return fail(GRFC_EINVAL, "grfc: sqrt-gamma table not set");
+  return GRFC_OK;
+}
+
+// Fields generated per accumulate launch: <= GRFC_COV_CHUNK and ~1 GiB of
+// scratch (GRFC_COV_BATCH overrides; results do not depend on it).
+static uint64_t cov_batch(grfc_plan p) {
+  const char* e = std::getenv("GRFC_COV_BATCH");
+  uint64_t b = e ? (uint64_t)std::strtoull(e, nullptr, 10) : 0;
+  if (!b) b = std::max<uint64_t>(1, (1ull << 30) / (p->points * dsize(p)));
+  return std::min<uint64_t>(b, GRFC_COV_CHUNK);
+}
+
+// Chunks [c0, c0 + nc): partial sums into part + (c - c0) * P, or, when
+// est != nullptr, merged into (est, comp) in chunk order through `acc`.
+static grfc_status cov_chunks(grfc_plan p, uint64_t seed, uint64_t samples, uint64_t c0, uint64_t nc, int64_t ref,
+                              double* part, double* acc, double* est, double* comp, cudaStream_t s,
+                              uint64_t* launches) {
+  const uint64_t P = p->points, B = cov_batch(p);
+  void* buf = nullptr;
+  GRFC_CUDA(cudaMallocAsync(&buf, (size_t)B * P * dsize(p), s));
+  grfc_status st = GRFC_OK;
+  for (uint64_t c = c0; c < c0 + nc && st == GRFC_OK; ++c) {
+    const uint64_t begin = c * GRFC_COV_CHUNK, end = std::min<uint64_t>(begin + GRFC_COV_CHUNK, samples);
+    double* a = est ? acc : part + (c - c0) * P;
+    cudaError_t e = cudaMemsetAsync(a, 0, P * sizeof(double), s);
+    for (uint64_t j = begin; j < end && e == cudaSuccess && st == GRFC_OK; j += B) {
+      const uint64_t n = std::min<uint64_t>(B, end - j);
+      st = grfc_generate(p, seed, j, n, buf, P, s);
+      *launches += t_launches;
+      if (st == GRFC_OK) e = launch_cov_accumulate(p->dtype, buf, n, P, P, (uint64_t)ref, a, s), ++*launches;
+    }
+    if (e == cudaSuccess && st == GRFC_OK && est) e = launch_cov_merge(a, est, comp, P, s), ++*launches;
+    if (e != cudaSuccess && st == GRFC_OK) st = fail(GRFC_ECUDA, std::string("CUDA: covariance: ") + cudaGetErrorString(e));
+  }
+  cudaFreeAsync(buf, s);
+  return st;
+}
+
+grfc_status grfc_covariance_accumulate(grfc_plan p, const void* d_fields, uint64_t nfields, uint64_t field_stride,
+                                       int64_t ref, double* d_acc, void* stream) {
+  t_launches = 0;
+  if (!p || !d_acc || (!d_fields && nfields)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (ref < 0 || (uint64_t)ref >= p->points)
+    return fail(GRFC_EINVAL, "estimate_covariance: reference index out of range");
+  if (field_stride < p->points && nfields > 1) return fail(GRFC_EINVAL, "grfc: field_stride < point count");
+  DeviceGuard guard(p->device);
+  GRFC_CUDA(launch_cov_accumulate(p->dtype, d_fields, nfields, field_stride, p->points, (uint64_t)ref, d_acc,
+                                  (cudaStream_t)stream));
+  return GRFC_OK;
+}
+
+grfc_status grfc_covariance_partials(grfc_plan p, uint64_t seed, uint64_t samples, uint64_t chunk0, uint64_t nchunks,
+                                     int64_t ref, double* d_partials, void* stream) {
+  grfc_status st = cov_check(p, samples, ref);
+  if (st != GRFC_OK) return st;
+  const uint64_t total = (samples + GRFC_COV_CHUNK - 1) / GRFC_COV_CHUNK;
+  if (chunk0 > total || nchunks > total - chunk0) return fail(GRFC_EINVAL, "grfc: chunk range out of range");
+  if (!d_partials && nchunks) return fail(GRFC_EINVAL, "grfc: null argument");
+  DeviceGuard guard(p->device);
+  uint64_t launches = 0;
+  st = cov_chunks(p, seed, samples, chunk0, nchunks, ref, d_partials, nullptr, nullptr, nullptr,
+                  (cudaStream_t)stream, &launches);
+  t_launches = launches;
+  return st;
+}
+
+grfc_status grfc_covariance_merge(grfc_plan p, const double* d_partials, uint64_t nchunks, uint64_t samples,
+                                  double* d_out, void* stream) {
+  t_launches = 0;
+  if (!p || !d_out || (!d_partials && nchunks)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (samples < 1) return fail(GRFC_EINVAL, "estimate_covariance: need at least one sample");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t P = p->points;
+  double* comp = nullptr;
+  GRFC_CUDA(cudaMallocAsync(&comp, P * sizeof(double), s));
+  cudaError_t e = cudaMemsetAsync(comp, 0, P * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, P * sizeof(double), s);
+  uint64_t launches = 0;
+  for (uint64_t c = 0; c < nchunks && e == cudaSuccess; ++c, ++launches)
+    e = launch_cov_merge(d_partials + c * P, d_out, comp, P, s);
+  if (e == cudaSuccess) e = launch_cov_scale(d_out, P, 1.0 / (double)samples, s), ++launches;
+  cudaFreeAsync(comp, s);
+  t_launches = launches;
+  GRFC_CUDA(e);
+  return GRFC_OK;
+}
+
+grfc_status grfc_estimate_covariance(grfc_plan p, uint64_t seed, uint64_t samples, int64_t ref, double* d_out,
+                                     void* stream) {
+  grfc_status st = cov_check(p, samples, ref);
+  if (st != GRFC_OK) return st;
+  if (!d_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t P = p->points;
+  double* scratch = nullptr;  // acc | comp
+  GRFC_CUDA(cudaMallocAsync(&scratch, 2 * P * sizeof(double), s));
+  cudaError_t e = cudaMemsetAsync(scratch + P, 0, P * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, P * sizeof(double), s);
+  uint64_t launches = 0;
+  if (e == cudaSuccess)
+    st = cov_chunks(p, seed, samples, 0, (samples + GRFC_COV_CHUNK - 1) / GRFC_COV_CHUNK, ref, nullptr, scratch,
+                    d_out, scratch + P, s, &launches);
+  if (e == cudaSuccess && st == GRFC_OK) e = launch_cov_scale(d_out, P, 1.0 / (double)samples, s), ++launches;
+  cudaFreeAsync(scratch, s);
+  t_launches = launches;
+  if (st != GRFC_OK) return st;
+  GRFC_CUDA(e);
+  return GRFC_OK;
+}
+
+grfc_status grfc_estimate_covariance_host(grfc_plan p, uint64_t seed, uint64_t samples, int64_t ref,
+                                          double* h_out) {
+  grfc_status st = cov_check(p, samples, ref);
+  if (st != GRFC_OK) return st;
+  if (!h_out) return fail(GRFC_EINVAL, "grfc: null argument");
+  DeviceGuard guard(p->device);
+  cudaStream_t s;
+  GRFC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, p->points * sizeof(double), s);
+  if (e == cudaSuccess) {
+    st = grfc_estimate_covariance(p, seed, samples, ref, d, s);
+    const uint64_t launches = t_launches;
+    if (st == GRFC_OK) e = cudaMemcpyAsync(h_out, d, p->points * sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    t_launches = launches;
+  }
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (st != GRFC_OK) return st;
+  GRFC_CUDA(e);
+  GRFC_CUDA(e2);
+  return GRFC_OK;
+}
+
+grfc_status grfc_covariance_chunk_injected_host(grfc_plan p, const double* draws, uint64_t nsamples,
+                                                uint64_t ndraws, int64_t ref, double* h_partial) {
+  if (!p || !h_partial || (!draws && nsamples)) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (ref < 0 || (uint64_t)ref >= p->points)
+    return fail(GRFC_EINVAL, "estimate_covariance: reference index out of range");
+  DeviceGuard guard(p->device);
+  cudaStream_t s;
+  GRFC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const uint64_t P = p->points, B = cov_batch(p);
+  void* buf = nullptr;
+  double* acc = nullptr;
+  grfc_status st = GRFC_OK;
+  cudaError_t e = cudaMallocAsync(&buf, (size_t)B * P * dsize(p), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&acc, P * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(acc, 0, P * sizeof(double), s);
+  uint64_t launches = 0;
+  for (uint64_t j = 0; j < nsamples && e == cudaSuccess && st == GRFC_OK; j += B) {
+    const uint64_t n = std::min<uint64_t>(B, nsamples - j);
+    for (uint64_t i = 0; i < n && st == GRFC_OK; ++i) {
+      st = grfc_generate_injected(p, draws + (j + i) * ndraws, ndraws, (char*)buf + i * P * dsize(p), s);
+      launches += t_launches;
+    }
+    if (st == GRFC_OK) e = launch_cov_accumulate(p->dtype, buf, n, P, P, (uint64_t)ref, acc, s), ++launches;
+  }
+  if (e == cudaSuccess && st == GRFC_OK)
+    e = cudaMemcpyAsync(h_partial, acc, P * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (buf) cudaFreeAsync(buf, s);
+  if (acc) cudaFreeAsync(acc, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  t_launches = launches;
+  if (st != GRFC_OK) return st;
+  GRFC_CUDA(e);
+  GRFC_CUDA(e2);
+  return GRFC_OK;
+}
+
 }  // extern "C"

@@ -115,6 +115,12 @@ def _load():
         "grfc_slab_sizes": [P, C.c_int, P, P, P],
         "grfc_slab_pass_a": [P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, P, P],
         "grfc_slab_pass_b": [P, C.c_int, P, P, P],
+        "grfc_estimate_covariance": [P, C.c_uint64, C.c_uint64, C.c_int64, P, P],
+        "grfc_estimate_covariance_host": [P, C.c_uint64, C.c_uint64, C.c_int64, P],
+        "grfc_covariance_partials": [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, P, P],
+        "grfc_covariance_merge": [P, P, C.c_uint64, C.c_uint64, P, P],
+        "grfc_covariance_accumulate": [P, P, C.c_uint64, C.c_uint64, C.c_int64, P, P],
+        "grfc_covariance_chunk_injected_host": [P, P, C.c_uint64, C.c_uint64, C.c_int64, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -136,8 +142,13 @@ EXPORTED = (
     "grfc_generate_injected", "grfc_half_noise_from_draws", "grfc_dump_noise", "grfc_dft_c2c", "grfc_plan_info",
     "grfc_last_launch_count", "grfc_kernel_timing_enable", "grfc_kernel_timing_read",
     "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps", "grfc_slab_sizes",
-    "grfc_slab_pass_a", "grfc_slab_pass_b",
+    "grfc_slab_pass_a", "grfc_slab_pass_b", "grfc_estimate_covariance", "grfc_estimate_covariance_host",
+    "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
+    "grfc_covariance_chunk_injected_host",
 )
+
+#: Samples per accumulation chunk of the covariance estimator (GRFC_COV_CHUNK; src/stats.cpp:18).
+COV_CHUNK = 1024
 
 
 def conjugate_reps(counts: Sequence[int]):
@@ -296,6 +307,75 @@ class Plan:
 
     def slab_pass_b(self, world: int, d_recv: int, d_out: int, stream: int = 0):
         _check(_lib.grfc_slab_pass_b(self._h, world, C.c_void_p(d_recv), C.c_void_p(d_out), C.c_void_p(stream)))
+
+    # ---- Monte-Carlo covariance (grf::estimate_covariance, src/stats.cpp:39-97)
+    def linear_index(self, index) -> int:
+        """Row-major linear index of a grid multi-index (GridSpec::linear_index)."""
+        if isinstance(index, (int, np.integer)):
+            return int(index)
+        lin = 0
+        for i, n in zip(index, self.counts):
+            lin = lin * n + int(i)
+        return lin
+
+    def estimate_covariance(self, seed: int, samples: int, reference, d_out: int, stream: int = 0):
+        _check(_lib.grfc_estimate_covariance(self._h, seed, samples, self.linear_index(reference), C.c_void_p(d_out),
+                                             C.c_void_p(stream)))
+
+    def estimate_covariance_host(self, seed: int, samples: int, reference) -> np.ndarray:
+        out = np.empty(self.points, dtype=np.float64)
+        _check(_lib.grfc_estimate_covariance_host(self._h, seed, samples, self.linear_index(reference),
+                                                  out.ctypes.data_as(C.c_void_p)))
+        return out.reshape(self.counts)
+
+    def covariance_partials(self, seed: int, samples: int, chunk0: int, nchunks: int, reference, d_partials: int,
+                            stream: int = 0):
+        _check(_lib.grfc_covariance_partials(self._h, seed, samples, chunk0, nchunks, self.linear_index(reference),
+                                             C.c_void_p(d_partials), C.c_void_p(stream)))
+
+    def covariance_merge(self, d_partials: int, nchunks: int, samples: int, d_out: int, stream: int = 0):
+        _check(_lib.grfc_covariance_merge(self._h, C.c_void_p(d_partials), nchunks, samples, C.c_void_p(d_out),
+                                          C.c_void_p(stream)))
+
+    def covariance_accumulate(self, d_fields: int, nfields: int, field_stride: int, reference, d_acc: int,
+                              stream: int = 0):
+        _check(_lib.grfc_covariance_accumulate(self._h, C.c_void_p(d_fields), nfields, field_stride,
+                                               self.linear_index(reference), C.c_void_p(d_acc), C.c_void_p(stream)))
+
+    def covariance_chunk_injected_host(self, draws: np.ndarray, reference) -> np.ndarray:
+        """Partial sum of one chunk whose samples are given as draw rows (reference draw order)."""
+        d = np.ascontiguousarray(draws, dtype=np.float64)
+        if d.ndim != 2:
+            raise ValueError("draws must be (nsamples, ndraws)")
+        out = np.empty(self.points, dtype=np.float64)
+        _check(_lib.grfc_covariance_chunk_injected_host(self._h, d.ctypes.data_as(C.c_void_p), d.shape[0], d.shape[1],
+                                                        self.linear_index(reference), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def estimate_covariance_tensor(self, seed: int, samples: int, reference, stream=None):
+        import torch
+
+        out = torch.empty(self.counts, dtype=torch.float64, device=f"cuda:{self.device}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.estimate_covariance(seed, samples, reference, out.data_ptr(), s.cuda_stream)
+        return out
+
+    def covariance_partials_tensor(self, seed: int, samples: int, chunk0: int, nchunks: int, reference, stream=None):
+        import torch
+
+        out = torch.empty((nchunks,) + self.counts, dtype=torch.float64, device=f"cuda:{self.device}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.covariance_partials(seed, samples, chunk0, nchunks, reference, out.data_ptr(), s.cuda_stream)
+        return out
+
+    def covariance_merge_tensor(self, partials, samples: int, stream=None):
+        import torch
+
+        p = partials.contiguous()
+        out = torch.empty(self.counts, dtype=torch.float64, device=p.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.covariance_merge(p.data_ptr(), p.shape[0], samples, out.data_ptr(), s.cuda_stream)
+        return out
 
     # ---- torch conveniences (torch is plumbing: device memory and streams)
     def generate_tensor(self, seed: int, first_field: int = 0, nfields: int = 1, out=None, stream=None):

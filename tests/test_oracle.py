@@ -180,3 +180,39 @@ def test_dft_round_trip_and_naive(port):
         assert np.abs(back - x).max() <= 1e-12 * np.abs(x).max()
         # numpy's ifftn * P is the exp(+) unnormalised sum
         np.testing.assert_allclose(fwd, np.fft.ifftn(x) * x.size, rtol=0, atol=1e-11 * np.abs(fwd).max())
+
+
+def estimate_covariance_restated(fields, ref_lin, samples, chunk=1024):
+    """numpy restatement of grf::estimate_covariance's arithmetic
+    (src/stats.cpp:60-96): per chunk, acc += f[ref] * f in sample order; chunk
+    partials merged in order with Kahan compensation; times 1/M."""
+    est = np.zeros(fields.shape[1])
+    comp = np.zeros_like(est)
+    for c0 in range(0, samples, chunk):
+        acc = np.zeros_like(est)
+        for j in range(c0, min(c0 + chunk, samples)):
+            acc = acc + fields[j, ref_lin] * fields[j]
+        y = acc - comp
+        t = est + y
+        comp = (t - est) - y
+        est = t
+    return est * (1.0 / samples)
+
+
+@pytest.mark.skipif(not po.reference_available(), reason="oracle/_ref not built")
+def test_covariance_estimator_restatement_matches_reference(port):
+    """The reference estimator (StreamFactory overload, FixedStream per sample)
+    equals the restated chunk/Kahan arithmetic on the port's fields; worker
+    count never changes a bit (test_stats.cpp:43-56)."""
+    ref = po.Reference()
+    counts, lengths = (6, 4), (1.0, 2.0)
+    dens = po.density("matern", 2, nu=1.5, ell=0.3)
+    M, refpt = 2100, (2, 1)
+    n = port.count_draws(counts, po.ONE_FFT_OVERWRITE)
+    draws = np.random.default_rng(3).standard_normal((M, n))
+    fields = np.stack([port.synthesize(counts, lengths, dens, po.ONE_FFT_OVERWRITE, d)[0].ravel() for d in draws])
+    want = estimate_covariance_restated(fields, refpt[0] * counts[1] + refpt[1], M)
+    a = ref.estimate_covariance_fixed(counts, lengths, dens, po.ONE_FFT_OVERWRITE, refpt, draws, threads=1).ravel()
+    b = ref.estimate_covariance_fixed(counts, lengths, dens, po.ONE_FFT_OVERWRITE, refpt, draws, threads=3).ravel()
+    assert np.array_equal(a, b)
+    assert np.abs(a - want).max() < 1e-13 * np.abs(want).max()
