@@ -187,6 +187,20 @@ grfc_status grfc_slab_pass_a(grfc_plan plan, int world, int rank, uint64_t seed,
                              void* stream);
 grfc_status grfc_slab_pass_b(grfc_plan plan, int world, const void* d_recv, void* d_out, void* stream);
 
+/* Plan grid: dim, counts[dim], lengths[dim], dtype and device (any output may be NULL). */
+grfc_status grfc_plan_grid(grfc_plan plan, int* dim, int64_t* counts, double* lengths, int* dtype, int* device);
+
+/* Batch GRF1 writer — the reference's write_grf1 (src/field_io.cpp:60-80,
+ * format include/grf/field_io.hpp:10-14: "GRF1" | u32 1 | u32 dim |
+ * (u64 N_i, f64 l_i)... | P f64, little-endian) applied to fields
+ * (seed, first_field + i), i < nfields, streamed device -> pinned host ->
+ * file with generation, copies and file writes overlapped. Field f goes to
+ * path_format with "{field}" replaced by f (required when nfields > 1).
+ * fp32 plans are widened exactly to f64. Synchronous. Errors: unopenable or
+ * short write -> GRFC_ERUNTIME with the reference's messages. */
+grfc_status grfc_write_grf1(grfc_plan plan, uint64_t seed, uint64_t first_field, uint64_t nfields,
+                            const char* path_format);
+
 /* Monte-Carlo covariance against one reference grid point — the device form
  * of grf::estimate_covariance (src/stats.cpp:39-97, include/grf/stats.hpp):
  *   est[K] = M^-1 sum_{j<M} f_j[ref] f_j[K],   f_j = field (seed, j) of grfc_generate

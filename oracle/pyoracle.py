@@ -233,5 +233,21 @@ class Reference(_Lib):
         return rows[:4 * n.value].reshape(n.value, 4), slope.value
 
 
+    def write_grf1(self, path, counts, lengths, values):
+        v = np.ascontiguousarray(values, np.float64).ravel()
+        self._check(self.lib.ref_write_grf1(str(path).encode(), len(counts), _i64(counts), _f64(lengths), _ptr(v)))
+
+    def read_grf1(self, path, cap=1 << 24):
+        dim = C.c_int(0)
+        counts = np.zeros(16, np.int64)
+        lengths = np.zeros(16)
+        vals = np.zeros(cap)
+        self._check(self.lib.ref_read_grf1(str(path).encode(), C.byref(dim), _ptr(counts, C.c_int64), _ptr(lengths),
+                                           _ptr(vals), C.c_uint64(cap)))
+        d = dim.value
+        P = int(np.prod(counts[:d]))
+        return tuple(int(c) for c in counts[:d]), tuple(lengths[:d]), vals[:P].reshape(counts[:d])
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_LIB)

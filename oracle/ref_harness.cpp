@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "grf/dft.hpp"
+#include "grf/field_io.hpp"
 #include "grf/hermitian.hpp"
 #include "grf/spectral.hpp"
 #include "grf/stats.hpp"
@@ -309,6 +310,29 @@ int ref_convergence_study(int level_min, int level_max, uint64_t samples, int al
       rows[4 * i + 3] = r.rows[i].mc_floor;
     }
     *slope = r.fitted_slope ? *r.fitted_slope : std::nan("");
+  });
+}
+
+// The reference's GRF1 writer / reader (src/field_io.cpp:60-107).
+int ref_write_grf1(const char* path, int dim, const int64_t* counts, const double* lengths, const double* values) {
+  return guarded([&] {
+    const grf::GridSpec grid = make_grid(dim, counts, lengths);
+    grf::RealField f{grid, std::vector<double>(values, values + grid.point_count()), {}, 0.0};
+    grf::write_grf1(path, f);
+  });
+}
+
+// Reads a GRF1 file: *dim, counts/lengths (up to 16), values (cap entries).
+int ref_read_grf1(const char* path, int* dim, int64_t* counts, double* lengths, double* values, uint64_t cap) {
+  return guarded([&] {
+    const grf::RealField f = grf::read_grf1(path);
+    *dim = f.grid.dim();
+    for (int a = 0; a < f.grid.dim(); ++a) {
+      counts[a] = f.grid.counts()[a];
+      lengths[a] = f.grid.lengths()[a];
+    }
+    if (f.values.size() > cap) throw std::runtime_error("ref_read_grf1: buffer too small");
+    std::memcpy(values, f.values.data(), sizeof(double) * f.values.size());
   });
 }
 

@@ -63,6 +63,8 @@ static grfc_status fail(grfc_status s, const std::string& msg) {
   return s;
 }
 
+grfc_status set_error(grfc_status s, const std::string& msg) { return fail(s, msg); }
+
 #define GRFC_CUDA(expr)                                                                   \
   do {                                                                                    \
     cudaError_t e_ = (expr);                                                              \
@@ -745,6 +747,18 @@ grfc_status grfc_slab_pass_b(grfc_plan p, int world, const void* d_recv, void* d
   if (!slab_geometry(p->fast3d, world, g)) return fail(GRFC_EINVAL, "grfc: world must divide N0 and N1");
   DeviceGuard guard(p->device);
   GRFC_CUDA(fast3d_pass_b(p->fast3d, world, d_recv, d_out, (cudaStream_t)stream));
+  return GRFC_OK;
+}
+
+grfc_status grfc_plan_grid(grfc_plan p, int* dim, int64_t* counts, double* lengths, int* dtype, int* device) {
+  if (!p) return fail(GRFC_EINVAL, "grfc: null argument");
+  if (dim) *dim = p->d;
+  for (int a = 0; a < p->d; ++a) {
+    if (counts) counts[a] = p->n[a];
+    if (lengths) lengths[a] = p->l[a];
+  }
+  if (dtype) *dtype = p->dtype;
+  if (device) *device = p->device;
   return GRFC_OK;
 }
 

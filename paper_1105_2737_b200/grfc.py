@@ -121,6 +121,8 @@ def _load():
         "grfc_covariance_merge": [P, P, C.c_uint64, C.c_uint64, P, P],
         "grfc_covariance_accumulate": [P, P, C.c_uint64, C.c_uint64, C.c_int64, P, P],
         "grfc_covariance_chunk_injected_host": [P, P, C.c_uint64, C.c_uint64, C.c_int64, P],
+        "grfc_plan_grid": [P, P, P, P, P, P],
+        "grfc_write_grf1": [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_char_p],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -144,11 +146,49 @@ EXPORTED = (
     "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps", "grfc_slab_sizes",
     "grfc_slab_pass_a", "grfc_slab_pass_b", "grfc_estimate_covariance", "grfc_estimate_covariance_host",
     "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
-    "grfc_covariance_chunk_injected_host",
+    "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1",
 )
 
 #: Samples per accumulation chunk of the covariance estimator (GRFC_COV_CHUNK; src/stats.cpp:18).
 COV_CHUNK = 1024
+
+
+def grf1_bytes(counts: Sequence[int], lengths: Sequence[float], values) -> bytes:
+    """GRF1 image (include/grf/field_io.hpp:10-14): "GRF1" | u32 1 | u32 d | (u64 N, f64 l)* | P f64, LE."""
+    import struct
+
+    head = b"GRF1" + struct.pack("<II", 1, len(counts))
+    head += b"".join(struct.pack("<Qd", int(n), float(l)) for n, l in zip(counts, lengths))
+    return head + np.ascontiguousarray(values, dtype="<f8").tobytes()
+
+
+def read_grf1(path):
+    """(counts, lengths, values) of a GRF1 file, validated like src/field_io.cpp:82-107."""
+    import struct
+
+    with open(path, "rb") as f:
+        data = f.read()
+    if len(data) < 12:
+        raise RuntimeError("read_grf1: truncated file")
+    if data[:4] != b"GRF1":
+        raise RuntimeError("read_grf1: bad magic")
+    version, d = struct.unpack_from("<II", data, 4)
+    if version != 1:
+        raise RuntimeError("read_grf1: unsupported version")
+    if not 1 <= d <= 16:
+        raise RuntimeError("read_grf1: implausible dimension")
+    off = 12 + 16 * d
+    if len(data) < off:
+        raise RuntimeError("read_grf1: truncated file")
+    axes = [struct.unpack_from("<Qd", data, 12 + 16 * a) for a in range(d)]
+    counts = tuple(int(n) for n, _ in axes)
+    lengths = tuple(float(l) for _, l in axes)
+    P = int(np.prod(counts))
+    if len(data) < off + 8 * P:
+        raise RuntimeError("read_grf1: truncated file")
+    if len(data) > off + 8 * P:
+        raise RuntimeError("read_grf1: trailing bytes after payload")
+    return counts, lengths, np.frombuffer(data, dtype="<f8", count=P, offset=off).reshape(counts)
 
 
 def conjugate_reps(counts: Sequence[int]):
@@ -307,6 +347,11 @@ class Plan:
 
     def slab_pass_b(self, world: int, d_recv: int, d_out: int, stream: int = 0):
         _check(_lib.grfc_slab_pass_b(self._h, world, C.c_void_p(d_recv), C.c_void_p(d_out), C.c_void_p(stream)))
+
+    # ---- GRF1 output (grf::write_grf1, src/field_io.cpp:60-80)
+    def write_grf1(self, seed: int, first_field: int, nfields: int, path_format: str):
+        """Fields (seed, first_field + i) -> one GRF1 file each; "{field}" in the path is the field index."""
+        _check(_lib.grfc_write_grf1(self._h, seed, first_field, nfields, str(path_format).encode()))
 
     # ---- Monte-Carlo covariance (grf::estimate_covariance, src/stats.cpp:39-97)
     def linear_index(self, index) -> int:

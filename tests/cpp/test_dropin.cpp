@@ -11,7 +11,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
+#include <sstream>
+#include <unistd.h>
 #include <functional>
 #include <numbers>
 #include <set>
@@ -20,7 +23,9 @@
 #include <vector>
 
 #include "grf/dft.hpp"
+#include "grf/field_io.hpp"
 #include "grf/hermitian.hpp"
+#include "grf/stats.hpp"
 #include "grf/synth.hpp"
 
 using namespace grf;
@@ -375,6 +380,168 @@ int main(int argc, char** argv) {
     CHECK(parse_algorithm("recursive") == Algorithm::one_fft_recursive);
     CHECK(!parse_algorithm("three-fft").has_value());
     CHECK(throws<std::invalid_argument>([&] { exact_discrete_covariance(g, ConstantDensity(1.0, 1), MultiIndex{8}); }));
+  });
+
+  run("estimator: rigged constant fields estimate to c^2 (test_stats.cpp:12-27)", [] {
+    const GridSpec g({1.0}, {8});
+    const ConstantDensity dens(4.0, 1);
+    const std::uint64_t nd = count_draws(g, Algorithm::one_fft_recursive);
+    const StreamFactory impulse = [nd](std::uint64_t) {
+      std::vector<double> v(static_cast<std::size_t>(nd), 0.0);
+      v[0] = 1.0;
+      return std::make_unique<FixedStream>(std::move(v));
+    };
+    const CovarianceEstimate e = estimate_covariance(g, dens, Algorithm::one_fft_recursive, 50, MultiIndex{3}, impulse);
+    const double c = std::sqrt(2.0 * std::numbers::pi * 4.0 / g.domain_volume());
+    bool ok = e.estimates.size() == 8 && e.sample_count == 50;
+    for (double v : e.estimates) ok = ok && near(v, c * c, 1e-12);
+    CHECK(ok);
+    const StreamFactory short_streams = [](std::uint64_t) { return std::make_unique<FixedStream>(std::vector<double>{1.0}); };
+    CHECK(throws<std::runtime_error>(
+        [&] { estimate_covariance(g, dens, Algorithm::one_fft_recursive, 5, MultiIndex{0}, short_streams); }));
+  });
+
+  run("estimator: flat density decorrelates off the reference (test_stats.cpp:29-41)", [] {
+    const GridSpec g({1.0}, {16});
+    const double c = 1.5;
+    const std::uint64_t m = 40000;
+    const CovarianceEstimate e = estimate_covariance(g, ConstantDensity(c, 1), Algorithm::two_fft, m, MultiIndex{0}, 17);
+    const double at0 = c * 2.0 * std::numbers::pi * 16.0 / g.domain_volume();
+    const double tol = 5.0 * at0 / std::sqrt(static_cast<double>(m));
+    CHECK(std::abs(e.estimates[0] - at0) < tol);
+    bool ok = true;
+    for (std::size_t i = 1; i < e.estimates.size(); ++i) ok = ok && std::abs(e.estimates[i]) < tol;
+    CHECK(ok);
+    CHECK(e.seed == 17);
+  });
+
+  run("estimator: reproducible for any worker count (test_stats.cpp:43-56)", [] {
+    const GridSpec g({2.0 * std::numbers::pi}, {16}, {-std::numbers::pi});
+    const Test1dDensity dens;
+    const auto a = estimate_covariance(g, dens, Algorithm::one_fft_overwrite, 3000, MultiIndex{8}, 9, 1);
+    const auto b = estimate_covariance(g, dens, Algorithm::one_fft_overwrite, 3000, MultiIndex{8}, 9, 4);
+    const auto c = estimate_covariance(g, dens, Algorithm::one_fft_overwrite, 3000, MultiIndex{8}, 9, 7);
+    CHECK(a.estimates == b.estimates && a.estimates == c.estimates);
+    CHECK(throws<std::invalid_argument>(
+        [&] { estimate_covariance(g, dens, Algorithm::two_fft, 0, MultiIndex{0}, 1); }));
+    CHECK(throws<std::invalid_argument>(
+        [&] { estimate_covariance(g, dens, Algorithm::two_fft, 10, MultiIndex{16}, 1); }));
+  });
+
+  run("max_error and slope fitting (test_stats.cpp:58-91)", [] {
+    const GridSpec g({1.0}, {4});
+    CovarianceEstimate e{g, {0}, {1.0, 2.0, 3.0, 4.0}, 1, 0};
+    const auto lin = [](std::span<const double> x) { return 10.0 * x[0]; };
+    CHECK(near(max_error(e, lin), 3.5, 1e-12));
+    const auto same = [&](std::span<const double> x) { return e.estimates[static_cast<std::size_t>(std::lround(x[0] * 4.0))]; };
+    CHECK(max_error(e, same) == 0.0);
+    const std::vector<double> x{2.0, 3.0, 4.0, 5.0};
+    std::vector<double> y;
+    for (double v : x) y.push_back(-4.0 * v);
+    const auto s = fit_slope(x, y);
+    CHECK(s.has_value() && near(*s, -4.0, 1e-12));
+    CHECK(!fit_slope(std::vector<double>{1.0}, std::vector<double>{2.0}).has_value());
+    CHECK(!fit_slope(std::vector<double>{1.0, 1.0}, std::vector<double>{1.0, 2.0}).has_value());
+  });
+
+  run("convergence study basics (test_stats.cpp:93-123)", [] {
+    CHECK(throws<std::invalid_argument>([] { convergence_study(1, 4, 100, Algorithm::two_fft, 0); }));
+    CHECK(throws<std::invalid_argument>([] { convergence_study(2, 13, 100, Algorithm::two_fft, 0); }));
+    CHECK(throws<std::invalid_argument>([] { convergence_study(5, 3, 100, Algorithm::two_fft, 0); }));
+    const ConvergenceReport one = convergence_study(2, 2, 400, Algorithm::one_fft_recursive, 12);
+    CHECK(one.rows.size() == 1 && one.rows[0].level == 2 && one.rows[0].cells == 4);
+    CHECK(near(one.rows[0].mc_floor, 0.1, 1e-12));
+    CHECK(!one.fitted_slope.has_value());
+    const ConvergenceReport r = convergence_study(2, 4, 10000, Algorithm::one_fft_recursive, 12);
+    CHECK(r.rows.size() == 3);
+    CHECK(r.rows[0].max_err > r.rows[1].max_err && r.rows[1].max_err > r.rows[2].max_err);
+    CHECK(std::abs(r.rows[0].max_err - 0.615) < 0.15 * 0.615);
+    CHECK(std::abs(r.rows[1].max_err - 0.328) < 0.2 * 0.328);
+    CHECK(std::abs(r.rows[2].max_err - 0.073) < 0.8 * 0.073);
+    CHECK(r.fitted_slope.has_value() && r.fitted_levels.size() == 3);
+  });
+
+  run("GRF1 round trip, header, corrupt files (test_field_io.cpp:41-92)", [] {
+    const auto tmp = std::filesystem::temp_directory_path() / ("grf_dropin_" + std::to_string(::getpid()));
+    const auto slurp = [](const std::filesystem::path& p) {
+      std::ifstream is(p, std::ios::binary);
+      std::ostringstream os;
+      os << is.rdbuf();
+      return os.str();
+    };
+    const auto spit = [](const std::filesystem::path& p, const std::string& b) {
+      std::ofstream os(p, std::ios::binary | std::ios::trunc);
+      os.write(b.data(), static_cast<std::streamsize>(b.size()));
+    };
+    const GridSpec grid({1.5, 2.0}, {4, 6});
+    const RealField field = synthesize(grid, PolyDecayDensity(1.0, 1, 1, 2, 2), 11, Algorithm::one_fft_recursive);
+    write_grf1(tmp, field);
+    const RealField back = read_grf1(tmp);
+    CHECK(back.grid.counts() == grid.counts() && back.grid.lengths() == grid.lengths());
+    CHECK(back.values.size() == field.values.size() &&
+          std::memcmp(back.values.data(), field.values.data(), 8 * field.values.size()) == 0);
+    write_grf1(tmp, RealField{GridSpec({1.0}, {2}), {0.5, -0.25}, {}, 0.0});
+    const std::string h = slurp(tmp);
+    CHECK(h.size() == 4 + 4 + 4 + 8 + 8 + 16 && h.substr(0, 4) == "GRF1" && h[4] == 1 && h[8] == 1 &&
+          static_cast<unsigned char>(h[12]) == 2);
+    write_grf1(tmp, RealField{GridSpec({1.0}, {4}), {1.0, 2.0, 3.0, 4.0}, {}, 0.0});
+    const std::string good = slurp(tmp);
+    spit(tmp, "GRG1" + good.substr(4));
+    bool magic = false;
+    try {
+      read_grf1(tmp);
+    } catch (const std::runtime_error& e) {
+      magic = std::string(e.what()) == "read_grf1: bad magic";
+    }
+    CHECK(magic);
+    std::string v2 = good;
+    v2[4] = 2;
+    spit(tmp, v2);
+    CHECK(throws<std::runtime_error>([&] { read_grf1(tmp); }));
+    spit(tmp, good.substr(0, good.size() - 3));
+    CHECK(throws<std::runtime_error>([&] { read_grf1(tmp); }));
+    spit(tmp, good + "x");
+    CHECK(throws<std::runtime_error>([&] { read_grf1(tmp); }));
+    CHECK(throws<std::runtime_error>([] { read_grf1("/nonexistent/grf1"); }));
+    // device batch writer: bit-exact with the same fields through RealField
+    const auto fmt = tmp.string() + "_{field}.grf1";
+    write_grf1_batch(grid, MaternDensity(1.5, 0.2, 2), 4, 10, 3, Algorithm::one_fft_overwrite, fmt);
+    const auto fields = synthesize_batch(grid, MaternDensity(1.5, 0.2, 2), 4, 10, 3, Algorithm::one_fft_overwrite);
+    for (int i = 0; i < 3; ++i) {
+      const auto p = tmp.string() + "_" + std::to_string(10 + i) + ".grf1";
+      CHECK(read_grf1(p).values == fields[static_cast<std::size_t>(i)].values);
+      std::filesystem::remove(p);
+    }
+    std::filesystem::remove(tmp);
+  });
+
+  run("PGM bytes and CSV dump (test_field_io.cpp:94-140)", [] {
+    const auto tmp = std::filesystem::temp_directory_path() / ("grf_pgm_" + std::to_string(::getpid()));
+    const GridSpec g({1.0, 1.0}, {2, 4});
+    write_field_pgm(tmp, RealField{g, {0, 1, 2, 3, 4, 5, 6, 7}, {}, 0.0});
+    std::ifstream is(tmp, std::ios::binary);
+    const std::string b((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    const std::string hdr = "P5\n4 2\n255\n";
+    const unsigned char want[8] = {0, 36, 73, 109, 146, 182, 219, 255};
+    bool ok = b.size() == hdr.size() + 8 && b.substr(0, hdr.size()) == hdr;
+    for (int i = 0; ok && i < 8; ++i) ok = static_cast<unsigned char>(b[hdr.size() + i]) == want[i];
+    CHECK(ok);
+    write_field_pgm(tmp, RealField{g, std::vector<double>(8, 3.0), {}, 0.0});
+    std::ifstream is2(tmp, std::ios::binary);
+    const std::string flat((std::istreambuf_iterator<char>(is2)), std::istreambuf_iterator<char>());
+    CHECK(flat.size() == hdr.size() + 8 && flat.substr(hdr.size()) == std::string(8, '\0'));
+    CHECK(throws<std::invalid_argument>([&] { write_field_pgm(tmp, RealField{GridSpec({1.0}, {4}), {1, 2, 3, 4}, {}, 0.0}); }));
+    std::filesystem::remove(tmp);
+    std::ostringstream os;
+    write_field_csv(os, RealField{GridSpec({1.0, 2.0}, {2, 2}, {0.0, 1.0}), {1.0, 2.0, 3.0, 4.5}, {}, 0.0});
+    std::istringstream in(os.str());
+    std::string line;
+    std::getline(in, line);
+    CHECK(line == "x1,x2,value");
+    int rows = 0;
+    bool commas = true;
+    while (std::getline(in, line)) ++rows, commas = commas && std::count(line.begin(), line.end(), ',') == 2;
+    CHECK(rows == 4 && commas && os.str().find("4.5") != std::string::npos);
   });
 
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
