@@ -347,6 +347,16 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
   int ndev = 0;
   GRFC_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(GRFC_EINVAL, "grfc: bad device ordinal");
+  {
+    // Stream-ordered scratch (ring, workspaces) comes from the device's default
+    // pool; keep freed blocks mapped so repeated calls reuse them instead of
+    // re-mapping tens of MB per call.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   DeviceGuard guard(device);
 
   std::unique_ptr<grfc_plan_s> p(new grfc_plan_s());

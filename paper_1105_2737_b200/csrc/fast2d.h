@@ -3,6 +3,8 @@
 // imaginary part of column 0, and an L2-resident half-spectrum intermediate.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -39,11 +41,21 @@ struct Fast2D {
 // a batch of nf fields; conc = resident CTAs.
 inline void ring_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, uint32_t* L, uint32_t* S,
                           uint32_t* conc) {
+  // lookahead = LA x (tiles all resident CTAs run at once) / (tiles per field);
+  // slots = lookahead + SL x that + 2. GRFC_RING_LA / GRFC_RING_SL override (A/B).
+  static const uint32_t la = [] {
+    const char* e = std::getenv("GRFC_RING_LA");
+    return e ? (uint32_t)std::atoi(e) : 8u;
+  }();
+  static const uint32_t sl = [] {
+    const char* e = std::getenv("GRFC_RING_SL");
+    return e ? (uint32_t)std::atoi(e) : 5u;
+  }();
   const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + rtiles);
-  uint32_t l = (4 * c + G - 1) / G;
+  uint32_t l = (la * c + G - 1) / G;
   l = l < 1 ? 1 : l;
   l = l < (uint32_t)nf ? l : (uint32_t)nf;
-  uint32_t s = l + 2 * ((c + G - 1) / G) + 2;
+  uint32_t s = l + sl * ((c + G - 1) / G) + 2;
   s = s < (uint32_t)nf ? s : (uint32_t)nf;
   *L = l;
   *S = s;

@@ -326,6 +326,14 @@ __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
 }
 
 // ---------------------------------------------------------------- tiles
+// Release-increment of a completion counter: orders this thread's (and, after
+// a CTA barrier, the CTA's) prior writes before the increment. Emits
+// MEMBAR.ALL.GPU + REDG — unlike __threadfence() + atomicAdd (MEMBAR.SC.GPU,
+// CCTL.IVALL, ATOMG) it neither invalidates L1 nor waits for a return value.
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -338,7 +346,8 @@ template <typename T, int N1, int ALG>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
-                                         const uint32_t* dep = nullptr, uint32_t dep_target = 0) {
+                                         const uint32_t* dep = nullptr, uint32_t dep_target = 0,
+                                         uint32_t* sig = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -399,6 +408,9 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     }
   }
   __syncthreads();
+  // Release of the CTA's previous tile: no global stores are in flight here,
+  // so the fence in front of the increment is cheap (persistent kernel).
+  if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
   C v[E];
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
@@ -454,7 +466,8 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 // real field rows out. Block = RPT * (M/E) threads.
 template <typename T, int M, int RPT>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
-                                         const C_t<T>* __restrict__ tw2, unsigned char* smem_raw) {
+                                         const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
+                                         uint32_t* sig = nullptr) {
   using C = C_t<T>;
   using PL = RowPlan<M, T>;
   constexpr int E = PL::E, TT = M / E;
@@ -469,6 +482,8 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
   for (int b = 0; b < E / R0; ++b)
 #pragma unroll
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcg(&Wr[j + b * TT + i * (M / R0)]);
+  // Release of the CTA's previous tile; its fence overlaps the W loads' latency.
+  if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
   RowEx<C> ex{reinterpret_cast<C*>(smem_raw) + (rl < RPT ? rl : 0) * row_pitch<M, C>(), rl < RPT};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
@@ -538,10 +553,7 @@ __device__ __forceinline__ void wait_geq(const uint32_t* ctr, uint32_t target) {
 
 __device__ __forceinline__ void signal_done(uint32_t* ctr) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-  }
+  if (threadIdx.x == 0) red_release_add(ctr, 1u);
 }
 
 // Resident CTAs per SM the fused kernel is compiled for (register budget):
@@ -564,67 +576,131 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   constexpr int RPT = rows_per_tile<N1, M, T>();
   const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
   if (table) fused2d_row_table<N1>(p, s_rowq);
-  // Thread 0 keeps one ticket in flight: the atomic for tile i+1 is issued
-  // when tile i starts, so its round trip overlaps tile i.
-  uint32_t next_ticket = 0;
-  if (threadIdx.x == 0) next_ticket = atomicAdd(q.ticket, 1u);
+  // One CTA barrier per tile. At the end of tile i thread 0 publishes ticket
+  // i+1 (its atomic was issued when tile i started, so the round trip hides
+  // behind tile i) together with whether i+1's dependency — its field's
+  // columns (row tile) or its ring slot's previous rows (column tile) — is
+  // already met; the barrier then both closes tile i and opens tile i+1.
+  // Thread 0 signals tile i's completion after that barrier; only if i+1's
+  // dependency was not yet met does it spin and add a second barrier.
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
   const uint32_t total = q.F * G;
+  struct Tile {
+    bool col;
+    uint32_t f, idx, slot, use;
+  };
+  auto decode = [&](uint32_t t) {
+    Tile x;
+    if (t < pro) {
+      x.col = true;
+      x.f = t / q.strips;
+      x.idx = t % q.strips;
+    } else if ((t -= pro) < nfull * G) {
+      const uint32_t g = t / G, r = t % G;
+      x.col = r < q.strips;
+      x.f = x.col ? g + q.L : g;
+      x.idx = x.col ? r : r - q.strips;
+    } else {
+      t -= nfull * G;
+      x.col = false;
+      x.f = nfull + t / q.rtiles;
+      x.idx = t % q.rtiles;
+    }
+    x.slot = x.f % q.S;
+    x.use = x.f / q.S;
+    return x;
+  };
+  // dependency counter / target of a tile (target 0: none)
+  auto dep_of = [&](const Tile& x, const uint32_t*& ctr) -> uint32_t {
+    ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
+    return x.col ? x.use * q.rtiles : (x.use + 1) * q.strips;
+  };
+  __shared__ uint32_t s_ready;
+  // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
+  // after, its atomic in flight). At the start of each tile it issues a
+  // relaxed load of tA's dependency counter, consumed at the end of the tile,
+  // so neither the ticket nor the readiness check costs an exposed round trip.
+  // (Reserving ahead cannot deadlock: every dependency points to a smaller
+  // ticket, and the smallest unfinished ticket is always a running tile.)
+  uint32_t tA = total, tB = total, dep_v = 0;
+  auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
+  // thread 0: readiness of ticket t given an (early) counter value v
+  auto ready_of = [&](uint32_t t, uint32_t v, bool recheck) -> uint32_t {
+    if (t >= total) return 1;
+    const Tile x = decode(t);
+    const uint32_t* ctr;
+    const uint32_t target = dep_of(x, ctr);
+    if (target == 0) return 1;
+    if (v < target && recheck) v = ld_relaxed_u32(ctr);
+    if (v < target) return 0;
+    // rows read what other CTAs wrote: acquire; a column tile's ring-slot reuse
+    // (write after the rows' reads) needs no L1-invalidating acquire
+    if (!x.col) (void)ld_acquire_u32(ctr);
+    return 1;
+  };
+  if (threadIdx.x == 0) {
+    const uint32_t t0 = claim();
+    tA = claim();
+    tB = claim();
+    s_ticket = t0;
+    s_ready = ready_of(t0, 0, true);
+  }
+  __syncthreads();
+  uint32_t* done_ctr = nullptr;  // thread 0: counter of the tile just finished
   long long c_col = 0, c_row = 0, c_wc = 0, c_wr = 0, c_tk = 0, n_col = 0, n_row = 0;
   for (;;) {
     long long t0 = q.stats ? clock64() : 0;
+    const uint32_t t = s_ticket;
+    const bool ready = s_ready;
     if (threadIdx.x == 0) {
-      s_ticket = next_ticket;
-      if (next_ticket < total) next_ticket = atomicAdd(q.ticket, 1u);
+      if (tA < total) {  // early dependency load of the next tile
+        const uint32_t* ctr;
+        dep_of(decode(tA), ctr);
+        dep_v = ld_relaxed_u32(ctr);
+      }
+    }
+    if (t >= total) break;
+    const Tile x = decode(t);
+    if (!ready) {  // rare: close the previous tile, wait for the dependency, one extra barrier
+      if (threadIdx.x == 0) {
+        if (done_ctr) red_release_add(done_ctr, 1u);
+        done_ctr = nullptr;
+        const uint32_t* ctr;
+        const uint32_t target = dep_of(x, ctr);
+        while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
+        if (!x.col) (void)ld_acquire_u32(ctr);
+      }
+      __syncthreads();
+    }
+    if (q.stats) (x.col ? c_wc : c_wr) += clock64() - t0;
+    long long b = q.stats ? clock64() : 0;
+    C_t<T>* Wf = ring + x.slot * slot_elems;
+    // the previous tile's completion is released inside this one (see col_tile / row_tile)
+    if (x.col) {
+      col_tile<T, N1, ALG>(p, key, field0 + x.f, (int)x.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
+                           nullptr, 0, done_ctr);
+      done_ctr = &q.col_done[x.slot];
+    } else {
+      row_tile<T, M, RPT>(Wf, (int)x.idx * RPT, N1, out + (int64_t)x.f * out_stride, tw2, smem_raw, done_ctr);
+      done_ctr = &q.row_done[x.slot];
+    }
+    // every tile has internal barriers, so all threads have read s_ticket / s_ready
+    long long e = q.stats ? clock64() : 0;
+    if (threadIdx.x == 0) {
+      s_ticket = tA;
+      s_ready = ready_of(tA, dep_v, true);
+      tA = tB;
+      tB = tB < total ? claim() : total;
     }
     __syncthreads();
-    uint32_t t = s_ticket;
-    if (q.stats) c_tk += clock64() - t0;
-    if (t >= total) break;
-    bool col;
-    uint32_t f, idx;
-    if (t < pro) {
-      col = true;
-      f = t / q.strips;
-      idx = t % q.strips;
-    } else if ((t -= pro) < nfull * G) {
-      const uint32_t g = t / G, r = t % G;
-      col = r < q.strips;
-      f = col ? g + q.L : g;
-      idx = col ? r : r - q.strips;
-    } else {
-      t -= nfull * G;
-      col = false;
-      f = nfull + t / q.rtiles;
-      idx = t % q.rtiles;
-    }
-    const uint32_t slot = f % q.S, use = f / q.S;
-    C_t<T>* Wf = ring + slot * slot_elems;
-    if (col) {
-      long long a = q.stats ? clock64() : 0;
-      long long b = a;
-      col_tile<T, N1, ALG>(p, key, field0 + f, (int)idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
-                           use ? &q.row_done[slot] : nullptr, use * q.rtiles);
-      signal_done(&q.col_done[slot]);
-      if (q.stats) {
-        c_wc += b - a;
-        c_col += clock64() - b;
-        ++n_col;
-      }
-    } else {
-      long long a = q.stats ? clock64() : 0;
-      wait_geq(&q.col_done[slot], (use + 1) * q.strips);
-      long long b = q.stats ? clock64() : 0;
-      row_tile<T, M, RPT>(Wf, (int)idx * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw);
-      signal_done(&q.row_done[slot]);
-      if (q.stats) {
-        c_wr += b - a;
-        c_row += clock64() - b;
-        ++n_row;
-      }
+    if (q.stats) {
+      (x.col ? c_col : c_row) += e - b;
+      c_tk += clock64() - e;
+      ++(x.col ? n_col : n_row);
     }
   }
+  if (threadIdx.x == 0 && done_ctr) red_release_add(done_ctr, 1u);  // the CTA's last tile
   if (q.stats && threadIdx.x == 0) {
     atomicAdd(&q.stats[0], (unsigned long long)c_col);
     atomicAdd(&q.stats[1], (unsigned long long)c_row);
