@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -314,6 +315,23 @@ def run_ours(args, cfg):
                     "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
                     "alg_bytes_per_launch": per_field * fields_per_launch,
                     "avg_launch_us": dms / dl * 1e3}
+    # compute-side diagnostic: nominal FFT flops 2.5 P log2 P per field (benchFFT
+    # convention, one C2R; Algorithm 1 would be 2x) against a measured FFMA2 peak, and which ceiling binds
+    compute = None
+    try:
+        fp32_peak = grfc.measure_fp32_peak(local)
+        flops = 2.5 * P * math.log2(P) * B
+        t_meas = ms / 1e3
+        t_hbm = B * P * s / (peak * 1e9)
+        t_fp = flops / (fp32_peak * 1e12)
+        compute = {"nominal_fft_tflops": flops / t_meas / 1e12, "fp32_peak_tflops": fp32_peak,
+                   "frac": flops / t_meas / 1e12 / fp32_peak, "t_hbm_us": t_hbm * 1e6, "t_fp32_us": t_fp * 1e6,
+                   "t_measured_us": t_meas * 1e6, "binding": "fp32" if t_fp > t_hbm else "hbm",
+                   "t_roof_frac": max(t_hbm, t_fp) / t_meas,
+                   "note": "peak = packed FFMA2 probe (grfc_measure_fp32_peak) on this GPU; the path also "
+                           "spends issue slots on Philox, Box-Muller, density and exchanges"}
+    except Exception as e:  # noqa: BLE001
+        compute = {"error": str(e)}
     path_gbs = B * P * s / (ms / 1e3) / 1e9
     kernels = {k: {"ms_per_step": v[0] / nsteps_timed, "launches_per_step": v[1] / nsteps_timed}
                for k, v in rows.items()}
@@ -370,7 +388,7 @@ def run_ours(args, cfg):
             "path_roofline": {"bound": "hbm", "achieved": path_gbs, "peak": peak, "unit": "GB/s",
                               "frac": path_gbs / peak,
                               "note": "compulsory P*s output bytes per field / whole-path time (SURVEY 8d)"},
-            "roofline": roofline, "kernels": kernels, "alg1": alg1, "e2e": e2e, "cpu_baseline": cpu,
+            "roofline": roofline, "compute_roofline": compute, "kernels": kernels, "alg1": alg1, "e2e": e2e, "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -243,6 +243,11 @@ grfc_status grfc_covariance_chunk_injected_host(grfc_plan plan, const double* dr
 grfc_status grfc_plan_info(grfc_plan plan, uint64_t* cells_half, uint64_t* points,
                            const char** path);
 
+/* Benchmark helper: measured dense FP32 throughput of `device` in TFLOP/s
+ * (packed FFMA2 chains on every SM; FMA = 2 flops) — the compute-roofline
+ * denominator bench.py reports beside the HBM one. */
+grfc_status grfc_measure_fp32_peak(int device, double* tflops);
+
 /* Number of kernel launches the last generate call on this thread issued. */
 uint64_t grfc_last_launch_count(void);
 

@@ -20,6 +20,8 @@
 //               double2 stores, 128 B per half-warp per instruction).
 #pragma once
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -204,6 +206,22 @@ struct ColEx {
   __device__ __forceinline__ C get(int e) const { return s[e * SLOTS + slot]; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
+
+// Column-strip exchange with one padding row-block every 16 rows (row e at
+// e + e/16): the stage-0 puts write rows 16 apart (stride R0 = 16), which
+// with SLOTS < 16 slots per row would hit the same banks 32/SLOTS times over;
+// at stride 17 row-blocks they spread across all banks. Needs
+// colx_rows(N) = N + N/16 rows of SLOTS elements.
+template <typename C, int SLOTS>
+struct ColExPad {
+  C* s;
+  int slot;
+  __device__ __forceinline__ static int row(int e) { return e + (e >> 4); }
+  __device__ __forceinline__ void put(int e, C v) { s[row(e) * SLOTS + slot] = v; }
+  __device__ __forceinline__ C get(int e) const { return s[row(e) * SLOTS + slot]; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+constexpr int colx_rows(int n) { return n + n / 16; }
 
 // Row exchange: row-contiguous, one pad element per 128 B (spreads the
 // stride-R writes of the first stage across banks).
@@ -417,7 +435,10 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[(j + b * TT + i * (N1 / R0)) * SLOTS + slot];
   __syncthreads();
-  ColEx<C, SLOTS> ex{sm, slot};
+  // padded exchange only where stage-0 conflicts are 8-way (SLOTS <= 4, N1 = 4096);
+  // at SLOTS = 8 the extra index arithmetic costs more than the 2-way conflicts
+  using Ex = std::conditional_t<(SLOTS <= 4), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
+  Ex ex{sm, slot};
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
 
   // The slot's previous field must be consumed before W is overwritten.
@@ -511,7 +532,7 @@ constexpr int rows_per_tile() {
 template <int N1, int M, typename T>
 constexpr size_t fused_smem() {
   using C = C_t<T>;
-  constexpr size_t a = (size_t)N1 * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t a = (size_t)(ColPlan<N1, T>::X <= 2 ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
   constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
   return a > b ? a : b;
 }
@@ -773,7 +794,7 @@ cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t
                                cudaStream_t s) {
   using C = C_t<T>;
   constexpr int CB = ColPlan<N1, T>::X;
-  const size_t smem = (size_t)N1 * 2 * CB * sizeof(C);
+  const size_t smem = (size_t)(CB <= 2 ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_cols_gen<T, N1, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -123,6 +123,7 @@ def _load():
         "grfc_covariance_chunk_injected_host": [P, P, C.c_uint64, C.c_uint64, C.c_int64, P],
         "grfc_plan_grid": [P, P, P, P, P, P],
         "grfc_write_grf1": [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_char_p],
+        "grfc_measure_fp32_peak": [C.c_int, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -146,8 +147,15 @@ EXPORTED = (
     "grfc_generate_injected_host", "grfc_dft_c2c_host", "grfc_conjugate_reps", "grfc_slab_sizes",
     "grfc_slab_pass_a", "grfc_slab_pass_b", "grfc_estimate_covariance", "grfc_estimate_covariance_host",
     "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
-    "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1",
+    "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1", "grfc_measure_fp32_peak",
 )
+
+
+def measure_fp32_peak(device: int = 0) -> float:
+    """Measured dense FP32 TFLOP/s of the device (FFMA2 probe)."""
+    v = C.c_double(0)
+    _check(_lib.grfc_measure_fp32_peak(device, C.byref(v)))
+    return v.value
 
 #: Samples per accumulation chunk of the covariance estimator (GRFC_COV_CHUNK; src/stats.cpp:18).
 COV_CHUNK = 1024
