@@ -37,7 +37,7 @@ __device__ __forceinline__ C_t<T> half_c(C_t<T> a) {
 template <typename T, int N1, int M, int RPT>
 __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int r0,
                                         C_t<T>* __restrict__ Wf, const C_t<T>* __restrict__ tw2,
-                                        unsigned char* smem_raw) {
+                                        unsigned char* smem_raw, uint32_t* sig = nullptr) {
   using C = C_t<T>;
   using PL = RowPlan<M, T>;
   constexpr int E = PL::E, TT = M / E, H = RPT / 2, PITCH = row_pitch<M, C>();
@@ -58,6 +58,7 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
     sm[(pr + H) * PITCH + RowEx<C>::pad(m)] = mk<C>(a1, b1);
   }
   __syncthreads();
+  if (sig && threadIdx.x == 0) red_release_add(sig, 1u);  // the CTA's previous tile
   const int tid = threadIdx.x, rl = tid / TT, j = tid % TT;
   const bool live = rl < RPT;
   const int rs = live ? rl : 0;
@@ -82,7 +83,8 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
 template <typename T, int N1>
 __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                               const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
-                                              unsigned char* smem_raw) {
+                                              unsigned char* smem_raw, const float* __restrict__ rowq,
+                                              uint32_t* sig = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -100,6 +102,7 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
     sm[j1 * SLOTS + slot] = __ldcg(&Wf[(int64_t)j1 * p.m + col]);
   }
   __syncthreads();
+  if (sig && threadIdx.x == 0) red_release_add(sig, 1u);  // the CTA's previous tile
   // 2. R2C split into the stage-0 registers
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
   C v[E];
@@ -131,8 +134,24 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
 #pragma unroll
     for (int i = 0; i < RL; ++i) sm[(j + b * TT + i * (N1 / RL)) * SLOTS + slot] = v[b * RL + i];
   __syncthreads();
-  // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col)
+  // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col).
+  // fp32 Matern / Gaussian interior columns: sqrt(g) from the per-CTA row table
+  // (fused2d_row_table; rowq is even in k1, so row -k1 reuses rowq[k1]) and the
+  // two columns' factors, as Algorithm 2's col_tile does.
   const T sc = (T)p.scale;
+  const bool fast_dens = sizeof(T) == 4 && rowq && !packed;
+  float Ac = 0.f, Ap = 0.f, Bc = 0.f, Bp = 0.f;
+  const bool matern = p.family == GRFC_DENSITY_MATERN;
+  if (fast_dens) {
+    const int pc = mid ? col : pcol;
+    const float wc = (float)(col <= p.n2 / 2 ? col : col - p.n2) * p.f_wstep2;
+    const float wp = (float)(pc <= p.n2 / 2 ? pc : pc - p.n2) * p.f_wstep2;
+    Ac = 1.0f + p.f_ell2 * wc * wc;
+    Ap = 1.0f + p.f_ell2 * wp * wp;
+    Bc = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wc * wc);
+    Bp = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wp * wp);
+  }
+  const float Km = p.f_sqrt_c * p.f_scale;
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
 #pragma unroll
@@ -146,6 +165,12 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
         const C FMm = mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half);
         Vk = cscale(F0k, sqrt_g2<T>(p, k1, 0) * sc);
         Vm = cscale(FMm, sqrt_g2<T>(p, km, p.m) * sc);
+      } else if (fast_dens) {
+        const float q = rowq[k1];
+        const float mk_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ac + q)) : Bc * q;
+        const float mm_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ap + q)) : Bp * q;
+        Vk = cscale(sm[k1 * SLOTS + slot], (T)mk_);
+        Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], (T)mm_);
       } else {
         Vk = cscale(sm[k1 * SLOTS + slot], sqrt_g2<T>(p, k1, col) * sc);
         Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], sqrt_g2<T>(p, km, mid ? col : pcol) * sc);
@@ -163,66 +188,132 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
     for (int i = 0; i < RL; ++i) __stcg(&Wf[(int64_t)(j + b * TT + i * (N1 / RL)) * p.m + col], v[b * RL + i]);
 }
 
+#ifndef GRFC_ALG1_MINB
+#define GRFC_ALG1_MINB 2
+#endif
+// Two resident 256-thread CTAs per SM for the fp32 shapes (<= 128 registers,
+// no spills at 512 x 256); larger blocks / fp64 let ptxas choose.
+template <int N1, int M, typename T>
+constexpr int alg1_min_blocks() {
+  return (sizeof(T) == 4 && fused_threads<N1, M, T>() <= 256) ? GRFC_ALG1_MINB : 0;
+}
 template <typename T, int N1, int M>
-__global__ void __launch_bounds__(fused_threads<N1, M, T>())
+__global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1, M, T>())
     k_fused2d_alg1(F2Params p, F2Sched3 q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring,
                    T* __restrict__ out, int64_t out_stride, const C_t<T>* __restrict__ tw1,
                    const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_ticket;
+  __shared__ uint32_t s_ticket, s_ready;
+  __shared__ float s_rowq[N1];
   constexpr int RPT = rows_per_tile<N1, M, T>();
+  const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
+  if (table) fused2d_row_table<N1>(p, s_rowq);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t L = q.L, F = q.F, g1 = q.g1, gc = q.gc, g2 = q.g2;
   // ticket ranges (L <= F/2): [0,L): R1 | [L,2L): R1 C | [2L,F): R1 C R2 | [F,F+L): C R2 | [F+L,F+2L): R2
   const uint32_t nA = L * g1, nB = L * (g1 + gc), nC = (F - 2 * L) * (g1 + gc + g2), nD = L * (gc + g2);
   const uint32_t total = F * (g1 + gc + g2);
-  uint32_t next_ticket = 0;
-  if (threadIdx.x == 0) next_ticket = atomicAdd(q.ticket, 1u);
-  for (;;) {
-    if (threadIdx.x == 0) {
-      s_ticket = next_ticket;
-      if (next_ticket < total) next_ticket = atomicAdd(q.ticket, 1u);
-    }
-    __syncthreads();
-    uint32_t t = s_ticket;
-    if (t >= total) break;
+  struct Tile {
     int kind;  // 0 R1, 1 C, 2 R2
-    uint32_t f, idx;
+    uint32_t f, idx, slot, use;
+  };
+  auto decode = [&](uint32_t t) {
+    Tile x;
     if (t < nA) {
-      kind = 0, f = t / g1, idx = t % g1;
+      x.kind = 0, x.f = t / g1, x.idx = t % g1;
     } else if ((t -= nA) < nB) {
       const uint32_t g = t / (g1 + gc), r = t % (g1 + gc);
-      if (r < g1) kind = 0, f = L + g, idx = r;
-      else kind = 1, f = g, idx = r - g1;
+      if (r < g1) x.kind = 0, x.f = L + g, x.idx = r;
+      else x.kind = 1, x.f = g, x.idx = r - g1;
     } else if ((t -= nB) < nC) {
       const uint32_t g = t / (g1 + gc + g2), r = t % (g1 + gc + g2);
-      if (r < g1) kind = 0, f = 2 * L + g, idx = r;
-      else if (r < g1 + gc) kind = 1, f = L + g, idx = r - g1;
-      else kind = 2, f = g, idx = r - g1 - gc;
+      if (r < g1) x.kind = 0, x.f = 2 * L + g, x.idx = r;
+      else if (r < g1 + gc) x.kind = 1, x.f = L + g, x.idx = r - g1;
+      else x.kind = 2, x.f = g, x.idx = r - g1 - gc;
     } else if ((t -= nC) < nD) {
       const uint32_t g = t / (gc + g2), r = t % (gc + g2);
-      if (r < gc) kind = 1, f = F - L + g, idx = r;
-      else kind = 2, f = F - 2 * L + g, idx = r - gc;
+      if (r < gc) x.kind = 1, x.f = F - L + g, x.idx = r;
+      else x.kind = 2, x.f = F - 2 * L + g, x.idx = r - gc;
     } else {
       t -= nD;
-      kind = 2, f = F - L + t / g2, idx = t % g2;
+      x.kind = 2, x.f = F - L + t / g2, x.idx = t % g2;
     }
-    const uint32_t slot = f % q.S, use = f / q.S;
-    C_t<T>* Wf = ring + slot * slot_elems;
-    if (kind == 0) {
-      wait_geq(&q.row_done[slot], use * g2);
-      r1_tile<T, N1, M, RPT>(p, key, field0 + f, (int)idx * (RPT / 2), Wf, tw2, smem_raw);
-      signal_done(&q.r1_done[slot]);
-    } else if (kind == 1) {
-      wait_geq(&q.r1_done[slot], (use + 1) * g1);
-      alg1_col_tile<T, N1>(p, (int)idx, Wf, tw1, tw2, smem_raw);
-      signal_done(&q.col_done[slot]);
-    } else {
-      wait_geq(&q.col_done[slot], (use + 1) * gc);
-      row_tile<T, M, RPT>(Wf, (int)idx * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw);
-      signal_done(&q.row_done[slot]);
-    }
+    x.slot = x.f % q.S;
+    x.use = x.f / q.S;
+    return x;
+  };
+  // dependency of a tile: R1 reuses the slot (rows of f - S consumed), C needs
+  // f's R1 tiles, R2 needs f's column tiles
+  auto dep_of = [&](const Tile& x, const uint32_t*& ctr) -> uint32_t {
+    if (x.kind == 0) return ctr = &q.row_done[x.slot], x.use * g2;
+    if (x.kind == 1) return ctr = &q.r1_done[x.slot], (x.use + 1) * g1;
+    return ctr = &q.col_done[x.slot], (x.use + 1) * gc;
+  };
+  // Same schedule as k_fused2d: one barrier per tile, two reserved tickets,
+  // early relaxed dependency loads, completion released inside the next tile.
+  uint32_t tA = total, tB = total, dep_v = 0;
+  auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
+  auto ready_of = [&](uint32_t t, uint32_t v) -> uint32_t {
+    if (t >= total) return 1;
+    const Tile x = decode(t);
+    const uint32_t* ctr;
+    const uint32_t target = dep_of(x, ctr);
+    if (target == 0) return 1;
+    if (v < target) v = ld_relaxed_u32(ctr);
+    if (v < target) return 0;
+    if (x.kind != 0) (void)ld_acquire_u32(ctr);
+    return 1;
+  };
+  if (threadIdx.x == 0) {
+    const uint32_t t0 = claim();
+    tA = claim();
+    tB = claim();
+    s_ticket = t0;
+    s_ready = ready_of(t0, 0);
   }
+  __syncthreads();
+  uint32_t* done_ctr = nullptr;
+  for (;;) {
+    const uint32_t t = s_ticket;
+    const bool ready = s_ready;
+    if (threadIdx.x == 0 && tA < total) {
+      const uint32_t* ctr;
+      dep_of(decode(tA), ctr);
+      dep_v = ld_relaxed_u32(ctr);
+    }
+    if (t >= total) break;
+    const Tile x = decode(t);
+    if (!ready) {
+      if (threadIdx.x == 0) {
+        if (done_ctr) red_release_add(done_ctr, 1u);
+        done_ctr = nullptr;
+        const uint32_t* ctr;
+        const uint32_t target = dep_of(x, ctr);
+        while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
+        if (x.kind != 0) (void)ld_acquire_u32(ctr);
+      }
+      __syncthreads();
+    }
+    C_t<T>* Wf = ring + x.slot * slot_elems;
+    if (x.kind == 0) {
+      r1_tile<T, N1, M, RPT>(p, key, field0 + x.f, (int)x.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr);
+      done_ctr = &q.r1_done[x.slot];
+    } else if (x.kind == 1) {
+      alg1_col_tile<T, N1>(p, (int)x.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, done_ctr);
+      done_ctr = &q.col_done[x.slot];
+    } else {
+      row_tile<T, M, RPT>(Wf, (int)x.idx * RPT, N1, out + (int64_t)x.f * out_stride, tw2, smem_raw, done_ctr);
+      done_ctr = &q.row_done[x.slot];
+    }
+    if (threadIdx.x == 0) {
+      s_ticket = tA;
+      s_ready = ready_of(tA, dep_v);
+      tA = tB;
+      tB = tB < total ? claim() : total;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && done_ctr) red_release_add(done_ctr, 1u);
 }
 
 inline size_t alg1_ctr_bytes(uint32_t S) { return ((1 + 3 * (size_t)S) * 4 + 255) / 256 * 256; }
@@ -230,10 +321,10 @@ inline size_t alg1_ctr_bytes(uint32_t S) { return ((1 + 3 * (size_t)S) * 4 + 255
 inline void alg1_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, uint32_t* L, uint32_t* S,
                           uint32_t* conc) {
   const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + 2 * rtiles);
-  uint32_t l = (3 * c + G - 1) / G;
+  uint32_t l = (5 * c + G - 1) / G;  // + the two tickets each CTA reserves ahead
   l = l < 1 ? 1 : l;
   l = l < (uint32_t)(nf / 2) ? l : (uint32_t)(nf / 2);
-  uint32_t s = 2 * l + 2 * ((c + G - 1) / G) + 2;
+  uint32_t s = 2 * l + 4 * ((c + G - 1) / G) + 2;
   s = s < (uint32_t)nf ? s : (uint32_t)nf;
   *L = l;
   *S = s;
