@@ -45,11 +45,11 @@ inline void ring_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, 
   // slots = lookahead + SL x that + 2. GRFC_RING_LA / GRFC_RING_SL override (A/B).
   static const uint32_t la = [] {
     const char* e = std::getenv("GRFC_RING_LA");
-    return e ? (uint32_t)std::atoi(e) : 8u;
+    return e ? (uint32_t)std::atoi(e) : 12u;
   }();
   static const uint32_t sl = [] {
     const char* e = std::getenv("GRFC_RING_SL");
-    return e ? (uint32_t)std::atoi(e) : 5u;
+    return e ? (uint32_t)std::atoi(e) : 8u;
   }();
   const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + rtiles);
   uint32_t l = (la * c + G - 1) / G;

@@ -578,10 +578,11 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 }
 
 // Resident CTAs per SM the fused kernel is compiled for (register budget):
-// tuned for the c2 shape (fp32 512 columns: 3 x 256 threads at 80 registers,
-// no spills); other shapes let ptxas choose.
+// tuned for the c2 shape (fp32 512 columns: 4 x 256 threads at 64 registers,
+// no spills; 3 CTAs at 80 registers measured 2% slower); other shapes let
+// ptxas choose.
 #ifndef GRFC_FUSED_MINB
-#define GRFC_FUSED_MINB 3
+#define GRFC_FUSED_MINB 4
 #endif
 template <int N1, int M, typename T>
 constexpr int fused_min_blocks() {
