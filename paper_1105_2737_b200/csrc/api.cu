@@ -800,8 +800,33 @@ static grfc_status cov_chunks(grfc_plan p, uint64_t seed, uint64_t samples, uint
                               uint64_t* launches) {
   const uint64_t P = p->points, B = cov_batch(p);
   void* buf = nullptr;
-  GRFC_CUDA(cudaMallocAsync(&buf, (size_t)B * P * dsize(p), s));
   grfc_status st = GRFC_OK;
+  // Small grids: whole groups of chunks per generate / accumulate / merge launch
+  // (k_cov_accumulate_chunks keeps every chunk's own ascending-j sum, and the
+  // grouped merge performs the same Kahan steps in chunk order: bit-identical).
+  const uint64_t chunk_bytes = (uint64_t)GRFC_COV_CHUNK * P * dsize(p);
+  const uint64_t G = std::getenv("GRFC_COV_BATCH") ? 1 : std::min<uint64_t>(nc, (1ull << 30) / chunk_bytes);
+  if (G >= 2) {
+    double* gpart = nullptr;
+    GRFC_CUDA(cudaMallocAsync(&buf, (size_t)(G * chunk_bytes), s));
+    cudaError_t e = est ? cudaMallocAsync(&gpart, (size_t)G * P * sizeof(double), s) : cudaSuccess;
+    for (uint64_t c = c0; c < c0 + nc && e == cudaSuccess && st == GRFC_OK; c += G) {
+      const uint64_t g = std::min<uint64_t>(G, c0 + nc - c);
+      const uint64_t begin = c * GRFC_COV_CHUNK, end = std::min<uint64_t>((c + g) * GRFC_COV_CHUNK, samples);
+      st = grfc_generate(p, seed, begin, end - begin, buf, P, s);
+      *launches += t_launches;
+      if (st != GRFC_OK) break;
+      double* out = est ? gpart : part + (c - c0) * P;
+      e = launch_cov_accumulate_chunks(p->dtype, buf, end - begin, P, (uint64_t)ref, GRFC_COV_CHUNK, out, s);
+      ++*launches;
+      if (e == cudaSuccess && est) e = launch_cov_merge_chunks(gpart, g, est, comp, P, s), ++*launches;
+    }
+    if (e != cudaSuccess && st == GRFC_OK) st = fail(GRFC_ECUDA, std::string("CUDA: covariance: ") + cudaGetErrorString(e));
+    if (gpart) cudaFreeAsync(gpart, s);
+    cudaFreeAsync(buf, s);
+    return st;
+  }
+  GRFC_CUDA(cudaMallocAsync(&buf, (size_t)B * P * dsize(p), s));
   for (uint64_t c = c0; c < c0 + nc && st == GRFC_OK; ++c) {
     const uint64_t begin = c * GRFC_COV_CHUNK, end = std::min<uint64_t>(begin + GRFC_COV_CHUNK, samples);
     double* a = est ? acc : part + (c - c0) * P;

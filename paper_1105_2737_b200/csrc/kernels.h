@@ -40,6 +40,10 @@ cudaError_t launch_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, u
 cudaError_t launch_cov_accumulate(int dtype, const void* fields, uint64_t nf, uint64_t stride, uint64_t P,
                                   uint64_t ref, double* acc, cudaStream_t s);
 cudaError_t launch_cov_merge(const double* acc, double* est, double* comp, uint64_t P, cudaStream_t s);
+cudaError_t launch_cov_accumulate_chunks(int dtype, const void* fields, uint64_t nf, uint64_t P, uint64_t ref,
+                                         uint64_t chunk, double* out, cudaStream_t s);
+cudaError_t launch_cov_merge_chunks(const double* part, uint64_t nchunks, double* est, double* comp, uint64_t P,
+                                    cudaStream_t s);
 cudaError_t launch_cov_scale(double* est, uint64_t P, double inv_m, cudaStream_t s);
 
 }  // namespace grfc
