@@ -89,7 +89,10 @@ GRFC_PLAN(ColPlan, 512, float, 32, 8, 32, 16)
 #endif
 GRFC_PLAN(ColPlan, 1024, float, 32, 8, 32, 32)
 GRFC_PLAN(ColPlan, 2048, float, 16, 4, 16, 16, 8)
-GRFC_PLAN(ColPlan, 4096, float, 16, 2, 16, 16, 16)
+#ifndef GRFC_COL4096_X
+#define GRFC_COL4096_X 2
+#endif
+GRFC_PLAN(ColPlan, 4096, float, 16, GRFC_COL4096_X, 16, 16, 16)
 GRFC_PLAN(ColPlan, 128, double, 16, 4, 16, 8)
 GRFC_PLAN(ColPlan, 256, double, 16, 8, 16, 16)
 GRFC_PLAN(ColPlan, 512, double, 16, 8, 16, 16, 2)
@@ -586,7 +589,9 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 #endif
 template <int N1, int M, typename T>
 constexpr int fused_min_blocks() {
-  return (N1 == 512 && sizeof(T) == 4) ? GRFC_FUSED_MINB : 0;
+  return (N1 == 512 && sizeof(T) == 4) ? GRFC_FUSED_MINB
+         : (N1 == 4096 && sizeof(T) == 4 && ColPlan<N1, T>::X == 1) ? 2
+                                                                    : 0;
 }
 template <typename T, int N1, int M, int ALG>
 __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1, M, T>())
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
     return x.col ? x.use * q.rtiles : (x.use + 1) * q.strips;
   };
-  __shared__ uint32_t s_ready;
+  __shared__ uint32_t s_ready, s_after;  // s_after: the ticket after s_ticket (L2 prefetch)
   // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
   // after, its atomic in flight). At the start of each tile it issues a
   // relaxed load of tA's dependency counter, consumed at the end of the tile,
@@ -666,6 +671,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     tA = claim();
     tB = claim();
     s_ticket = t0;
+    s_after = tA;
     s_ready = ready_of(t0, 0, true);
   }
   __syncthreads();
@@ -684,6 +690,20 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     }
     if (t >= total) break;
     const Tile x = decode(t);
+    {
+      // If the tile after this one is a row tile, pull its W rows toward L2 now
+      // (one 128-byte line per thread and pass); the ring is larger than L2.
+      const uint32_t ta = s_after;
+      if (ta < total) {
+        const Tile y = decode(ta);
+        if (!y.col) {
+          const char* base = reinterpret_cast<const char*>(ring + y.slot * slot_elems + (uint64_t)y.idx * RPT * M);
+          constexpr uint32_t lines = (uint32_t)((uint64_t)RPT * M * sizeof(C_t<T>) / 128);
+          for (uint32_t l = threadIdx.x; l < lines; l += blockDim.x)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (uint64_t)l * 128));
+        }
+      }
+    }
     if (!ready) {  // rare: close the previous tile, wait for the dependency, one extra barrier
       if (threadIdx.x == 0) {
         if (done_ctr) red_release_add(done_ctr, 1u);
@@ -711,6 +731,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     long long e = q.stats ? clock64() : 0;
     if (threadIdx.x == 0) {
       s_ticket = tA;
+      s_after = tB;
       s_ready = ready_of(tA, dep_v, true);
       tA = tB;
       tB = tB < total ? claim() : total;
