@@ -598,7 +598,6 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     k_fused2d(F2Params p, F2Sched q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring, T* __restrict__ out,
               int64_t out_stride, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_ticket;
   __shared__ float s_rowq[N1];
   constexpr int RPT = rows_per_tile<N1, M, T>();
   const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
@@ -643,44 +642,59 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
     return x.col ? x.use * q.rtiles : (x.use + 1) * q.strips;
   };
-  __shared__ uint32_t s_ready, s_after;  // s_after: the ticket after s_ticket (L2 prefetch)
   // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
   // after, its atomic in flight). At the start of each tile it issues a
   // relaxed load of tA's dependency counter, consumed at the end of the tile,
   // so neither the ticket nor the readiness check costs an exposed round trip.
   // (Reserving ahead cannot deadlock: every dependency points to a smaller
   // ticket, and the smallest unfinished ticket is always a running tile.)
+  // Thread 0 also decodes the tiles (integer divisions) and publishes them in
+  // shared memory, so the other threads only read the message.
+  struct Msg {
+    uint32_t t, ready, col, f, idx, slot, pf;
+    uint64_t pf_off;  // element offset of the W rows of the tile after next (pf: it is a row tile)
+  };
+  __shared__ Msg s_msg;
   uint32_t tA = total, tB = total, dep_v = 0;
   auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
-  // thread 0: readiness of ticket t given an (early) counter value v
-  auto ready_of = [&](uint32_t t, uint32_t v, bool recheck) -> uint32_t {
-    if (t >= total) return 1;
-    const Tile x = decode(t);
-    const uint32_t* ctr;
-    const uint32_t target = dep_of(x, ctr);
-    if (target == 0) return 1;
-    if (v < target && recheck) v = ld_relaxed_u32(ctr);
-    if (v < target) return 0;
-    // rows read what other CTAs wrote: acquire; a column tile's ring-slot reuse
-    // (write after the rows' reads) needs no L1-invalidating acquire
-    if (!x.col) (void)ld_acquire_u32(ctr);
-    return 1;
+  // thread 0: message for ticket t (readiness from the early counter value v)
+  // plus the prefetch target of ticket t2
+  auto publish = [&](uint32_t t, uint32_t v, uint32_t t2) {
+    Msg m{};
+    m.t = t;
+    m.ready = 1;
+    if (t < total) {
+      const Tile x = decode(t);
+      m.col = x.col, m.f = x.f, m.idx = x.idx, m.slot = x.slot;
+      const uint32_t* ctr;
+      const uint32_t target = dep_of(x, ctr);
+      if (target) {
+        if (v < target) v = ld_relaxed_u32(ctr);
+        m.ready = v >= target;
+        // rows read what other CTAs wrote: acquire; a column tile's ring-slot reuse
+        // (write after the rows' reads) needs no L1-invalidating acquire
+        if (m.ready && !x.col) (void)ld_acquire_u32(ctr);
+      }
+    }
+    if (t2 < total) {
+      const Tile y = decode(t2);
+      m.pf = !y.col;
+      m.pf_off = y.slot * slot_elems + (uint64_t)y.idx * RPT * M;
+    }
+    s_msg = m;
   };
   if (threadIdx.x == 0) {
     const uint32_t t0 = claim();
     tA = claim();
     tB = claim();
-    s_ticket = t0;
-    s_after = tA;
-    s_ready = ready_of(t0, 0, true);
+    publish(t0, 0, tA);
   }
   __syncthreads();
   uint32_t* done_ctr = nullptr;  // thread 0: counter of the tile just finished
   long long c_col = 0, c_row = 0, c_wc = 0, c_wr = 0, c_tk = 0, n_col = 0, n_row = 0;
   for (;;) {
     long long t0 = q.stats ? clock64() : 0;
-    const uint32_t t = s_ticket;
-    const bool ready = s_ready;
+    const Msg m = s_msg;
     if (threadIdx.x == 0) {
       if (tA < total) {  // early dependency load of the next tile
         const uint32_t* ctr;
@@ -688,59 +702,50 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
         dep_v = ld_relaxed_u32(ctr);
       }
     }
-    if (t >= total) break;
-    const Tile x = decode(t);
-    {
-      // If the tile after this one is a row tile, pull its W rows toward L2 now
-      // (one 128-byte line per thread and pass); the ring is larger than L2.
-      const uint32_t ta = s_after;
-      if (ta < total) {
-        const Tile y = decode(ta);
-        if (!y.col) {
-          const char* base = reinterpret_cast<const char*>(ring + y.slot * slot_elems + (uint64_t)y.idx * RPT * M);
-          constexpr uint32_t lines = (uint32_t)((uint64_t)RPT * M * sizeof(C_t<T>) / 128);
-          for (uint32_t l = threadIdx.x; l < lines; l += blockDim.x)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (uint64_t)l * 128));
-        }
-      }
+    if (m.t >= total) break;
+    if (m.pf) {
+      // the tile after this one is a row tile: pull its W rows toward L2 now
+      // (one 128-byte line per thread and pass); the ring is larger than L2
+      const char* base = reinterpret_cast<const char*>(ring + m.pf_off);
+      constexpr uint32_t lines = (uint32_t)((uint64_t)RPT * M * sizeof(C_t<T>) / 128);
+      for (uint32_t l = threadIdx.x; l < lines; l += blockDim.x)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (uint64_t)l * 128));
     }
-    if (!ready) {  // rare: close the previous tile, wait for the dependency, one extra barrier
+    if (!m.ready) {  // rare: close the previous tile, wait for the dependency, one extra barrier
       if (threadIdx.x == 0) {
         if (done_ctr) red_release_add(done_ctr, 1u);
         done_ctr = nullptr;
         const uint32_t* ctr;
-        const uint32_t target = dep_of(x, ctr);
+        const uint32_t target = dep_of(decode(m.t), ctr);
         while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
-        if (!x.col) (void)ld_acquire_u32(ctr);
+        if (!m.col) (void)ld_acquire_u32(ctr);
       }
       __syncthreads();
     }
-    if (q.stats) (x.col ? c_wc : c_wr) += clock64() - t0;
+    if (q.stats) (m.col ? c_wc : c_wr) += clock64() - t0;
     long long b = q.stats ? clock64() : 0;
-    C_t<T>* Wf = ring + x.slot * slot_elems;
+    C_t<T>* Wf = ring + m.slot * slot_elems;
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
-    if (x.col) {
-      col_tile<T, N1, ALG>(p, key, field0 + x.f, (int)x.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
+    if (m.col) {
+      col_tile<T, N1, ALG>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
                            nullptr, 0, done_ctr);
-      done_ctr = &q.col_done[x.slot];
+      done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT>(Wf, (int)x.idx * RPT, N1, out + (int64_t)x.f * out_stride, tw2, smem_raw, done_ctr);
-      done_ctr = &q.row_done[x.slot];
+      row_tile<T, M, RPT>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
+      done_ctr = &q.row_done[m.slot];
     }
-    // every tile has internal barriers, so all threads have read s_ticket / s_ready
+    // every tile has internal barriers, so all threads have read s_msg
     long long e = q.stats ? clock64() : 0;
     if (threadIdx.x == 0) {
-      s_ticket = tA;
-      s_after = tB;
-      s_ready = ready_of(tA, dep_v, true);
+      publish(tA, dep_v, tB);
       tA = tB;
       tB = tB < total ? claim() : total;
     }
     __syncthreads();
     if (q.stats) {
-      (x.col ? c_col : c_row) += e - b;
+      (m.col ? c_col : c_row) += e - b;
       c_tk += clock64() - e;
-      ++(x.col ? n_col : n_row);
+      ++(m.col ? n_col : n_row);
     }
   }
   if (threadIdx.x == 0 && done_ctr) red_release_add(done_ctr, 1u);  // the CTA's last tile
