@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
                    T* __restrict__ out, int64_t out_stride, const C_t<T>* __restrict__ tw1,
                    const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_ticket, s_ready;
   __shared__ float s_rowq[N1];
   constexpr int RPT = rows_per_tile<N1, M, T>();
   const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
@@ -253,61 +252,68 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
   // early relaxed dependency loads, completion released inside the next tile.
   uint32_t tA = total, tB = total, dep_v = 0;
   auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
-  auto ready_of = [&](uint32_t t, uint32_t v) -> uint32_t {
-    if (t >= total) return 1;
-    const Tile x = decode(t);
-    const uint32_t* ctr;
-    const uint32_t target = dep_of(x, ctr);
-    if (target == 0) return 1;
-    if (v < target) v = ld_relaxed_u32(ctr);
-    if (v < target) return 0;
-    if (x.kind != 0) (void)ld_acquire_u32(ctr);
-    return 1;
+  // thread 0 decodes (integer divisions) and publishes the next tile
+  struct Msg {
+    uint32_t t, ready, kind, f, idx, slot;
+  };
+  __shared__ Msg s_msg;
+  auto publish = [&](uint32_t t, uint32_t v) {
+    Msg m{};
+    m.t = t;
+    m.ready = 1;
+    if (t < total) {
+      const Tile x = decode(t);
+      m.kind = (uint32_t)x.kind, m.f = x.f, m.idx = x.idx, m.slot = x.slot;
+      const uint32_t* ctr;
+      const uint32_t target = dep_of(x, ctr);
+      if (target) {
+        if (v < target) v = ld_relaxed_u32(ctr);
+        m.ready = v >= target;
+        if (m.ready && x.kind != 0) (void)ld_acquire_u32(ctr);
+      }
+    }
+    s_msg = m;
   };
   if (threadIdx.x == 0) {
     const uint32_t t0 = claim();
     tA = claim();
     tB = claim();
-    s_ticket = t0;
-    s_ready = ready_of(t0, 0);
+    publish(t0, 0);
   }
   __syncthreads();
   uint32_t* done_ctr = nullptr;
   for (;;) {
-    const uint32_t t = s_ticket;
-    const bool ready = s_ready;
+    const Msg m = s_msg;
     if (threadIdx.x == 0 && tA < total) {
       const uint32_t* ctr;
       dep_of(decode(tA), ctr);
       dep_v = ld_relaxed_u32(ctr);
     }
-    if (t >= total) break;
-    const Tile x = decode(t);
-    if (!ready) {
+    if (m.t >= total) break;
+    if (!m.ready) {
       if (threadIdx.x == 0) {
         if (done_ctr) red_release_add(done_ctr, 1u);
         done_ctr = nullptr;
         const uint32_t* ctr;
-        const uint32_t target = dep_of(x, ctr);
+        const uint32_t target = dep_of(decode(m.t), ctr);
         while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
-        if (x.kind != 0) (void)ld_acquire_u32(ctr);
+        if (m.kind != 0) (void)ld_acquire_u32(ctr);
       }
       __syncthreads();
     }
-    C_t<T>* Wf = ring + x.slot * slot_elems;
-    if (x.kind == 0) {
-      r1_tile<T, N1, M, RPT>(p, key, field0 + x.f, (int)x.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr);
-      done_ctr = &q.r1_done[x.slot];
-    } else if (x.kind == 1) {
-      alg1_col_tile<T, N1>(p, (int)x.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, done_ctr);
-      done_ctr = &q.col_done[x.slot];
+    C_t<T>* Wf = ring + m.slot * slot_elems;
+    if (m.kind == 0) {
+      r1_tile<T, N1, M, RPT>(p, key, field0 + m.f, (int)m.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr);
+      done_ctr = &q.r1_done[m.slot];
+    } else if (m.kind == 1) {
+      alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, done_ctr);
+      done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT>(Wf, (int)x.idx * RPT, N1, out + (int64_t)x.f * out_stride, tw2, smem_raw, done_ctr);
-      done_ctr = &q.row_done[x.slot];
+      row_tile<T, M, RPT>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
+      done_ctr = &q.row_done[m.slot];
     }
     if (threadIdx.x == 0) {
-      s_ticket = tA;
-      s_ready = ready_of(tA, dep_v);
+      publish(tA, dep_v);
       tA = tB;
       tB = tB < total ? claim() : total;
     }
