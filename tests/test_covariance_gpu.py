@@ -125,3 +125,13 @@ def test_statistical_gate_through_estimator(ref):
         est = plan.estimate_covariance_host(123, M, (0, 0))
         tol = 5 * 2 / math.sqrt(M) * exact.flat[0]
         assert np.abs(est - exact).max() < tol, (alg, np.abs(est - exact).max(), tol)
+
+
+def test_distributed_helper_single_rank_matches_estimate():
+    """paper_1105_2737_b200.dist on one rank (no process group): device partials +
+    device merge == grfc_estimate_covariance, bit for bit."""
+    from paper_1105_2737_b200 import dist as gd
+
+    plan = grfc.Plan((128, 64), (1.0, 1.0), grfc.Density.matern(2, 1.5, 0.1), grfc.ONE_FFT_OVERWRITE, grfc.F64)
+    est = gd.estimate_covariance_distributed(plan, 3, 2500, (5, 9))
+    assert torch.equal(est.reshape(plan.counts), plan.estimate_covariance_tensor(3, 2500, (5, 9)))
