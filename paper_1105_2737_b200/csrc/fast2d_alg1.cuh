@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
       alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, done_ctr);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
       done_ctr = &q.row_done[m.slot];
     }
     if (threadIdx.x == 0) {

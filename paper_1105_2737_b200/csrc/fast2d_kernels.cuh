@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -127,6 +128,15 @@ constexpr int row_threads() {
 // Stage (radix R, NS = product of the earlier radices): thread j runs E/R
 // butterflies jj = j + b*TT on inputs x[jj + i N/R], twiddled by
 // w_{NS R}^{i (jj mod NS)}; outputs go to (jj/NS) NS R + jj%NS + i NS.
+// fp32 stage twiddles w^i (i = 1..R-1): the power-of-two powers are loaded,
+// the others formed as w^i = w^hb(i) w^(i - hb(i)) (hb = highest power of two
+// <= i; at most 3 products deep for R <= 16): R-1-log2 R complex multiplies
+// (2 packed instructions each) replace the loads and their address arithmetic.
+#ifndef GRFC_TWREC
+#define GRFC_TWREC 1
+#endif
+constexpr int hibit(int i) { return i >= 16 ? 16 : i >= 8 ? 8 : i >= 4 ? 4 : i >= 2 ? 2 : 1; }
+
 template <int N, int E, int R, int NS, int SIGN, typename C>
 __device__ __forceinline__ void stage_compute(C* v, int j, const C* __restrict__ tw, int tws) {
   constexpr int TT = N / E;
@@ -134,11 +144,26 @@ __device__ __forceinline__ void stage_compute(C* v, int j, const C* __restrict__
   for (int b = 0; b < E / R; ++b) {
     if constexpr (NS > 1) {
       const int k = (j + b * TT) % NS;
+      if constexpr (GRFC_TWREC && sizeof(C) == 8 && R >= 4 && R <= 32) {
+        C w[R];
+        Unroll<1, R>::run([&](auto ii) {
+          constexpr int i = decltype(ii)::value;
+          constexpr int hb = hibit(i);
+          if constexpr (hb == i) {
+            w[i] = __ldg(&tw[(i * k * (N / (NS * R))) * tws]);
+            if (SIGN < 0) w[i].y = -w[i].y;
+          } else {
+            w[i] = cmul(w[hb], w[i - hb]);
+          }
+          v[b * R + i] = cmul(v[b * R + i], w[i]);
+        });
+      } else {
 #pragma unroll
-      for (int i = 1; i < R; ++i) {
-        C w = __ldg(&tw[(i * k * (N / (NS * R))) * tws]);
-        if (SIGN < 0) w.y = -w.y;
-        v[b * R + i] = cmul(v[b * R + i], w);
+        for (int i = 1; i < R; ++i) {
+          C w = __ldg(&tw[(i * k * (N / (NS * R))) * tws]);
+          if (SIGN < 0) w.y = -w.y;
+          v[b * R + i] = cmul(v[b * R + i], w);
+        }
       }
     }
     dft<R, SIGN>(&v[b * R]);
@@ -158,6 +183,34 @@ __device__ __forceinline__ int stage_in_index(int j, int b, int i) {
   return j + b * TT + i * (N / R);
 }
 
+// Exchange addressing. An exchange type may provide put2(base, off, v) /
+// get2(base, off) taking the element index split into a runtime per-butterfly
+// base and a compile-time offset, so the shared-memory address is one base
+// register plus an immediate (with the pow2 padding rules used here,
+// pad(base + off) = pad(base) + pad(off) for every stage: see RowEx).
+template <typename Ex, typename = void>
+struct HasPut2 : std::false_type {};
+#ifndef GRFC_EX2
+#define GRFC_EX2 1
+#endif
+template <typename Ex>
+struct HasPut2<Ex, std::void_t<decltype(&Ex::template put2<0>)>> : std::bool_constant<GRFC_EX2 != 0> {};
+
+template <int OFF, typename Ex, typename C>
+__device__ __forceinline__ void ex_put(Ex& ex, int base, C v) {
+  if constexpr (HasPut2<Ex>::value)
+    ex.template put2<OFF>(base, v);
+  else
+    ex.put(base + OFF, v);
+}
+template <int OFF, typename C, typename Ex>
+__device__ __forceinline__ C ex_get(const Ex& ex, int base) {
+  if constexpr (HasPut2<Ex>::value)
+    return ex.template get2<OFF>(base);
+  else
+    return ex.get(base + OFF);
+}
+
 // Runs the stages on v (stage-0 inputs already in v, ordered b*R0 + i).
 // Exchanges go through `ex`. On return v[b*RL + i] holds output element
 // j + b*TT + i*N/RL (RL the last radix).
@@ -166,15 +219,25 @@ __device__ __forceinline__ void run_stages(C* v, int j, const C* __restrict__ tw
   stage_compute<N, E, R, NS, SIGN>(v, j, tw, tws);
   if constexpr (sizeof...(Rest) > 0) {
     constexpr int R2 = RFirst<Radices<Rest...>>::value;
+    constexpr int TT = N / E;
 #pragma unroll
-    for (int b = 0; b < E / R; ++b)
-#pragma unroll
-      for (int i = 0; i < R; ++i) ex.put(stage_out_index<N, E, R, NS>(j, b, i), v[b * R + i]);
+    for (int b = 0; b < E / R; ++b) {
+      const int jj = j + b * TT;
+      const int base = (jj / NS) * NS * R + (jj % NS);
+      Unroll<0, R>::run([&](auto ii) {
+        constexpr int i = decltype(ii)::value;
+        ex_put<i * NS>(ex, base, v[b * R + i]);
+      });
+    }
     ex.sync();
 #pragma unroll
-    for (int b = 0; b < E / R2; ++b)
-#pragma unroll
-      for (int i = 0; i < R2; ++i) v[b * R2 + i] = ex.get(stage_in_index<N, E, R2>(j, b, i));
+    for (int b = 0; b < E / R2; ++b) {
+      const int base = j + b * TT;
+      Unroll<0, R2>::run([&](auto ii) {
+        constexpr int i = decltype(ii)::value;
+        v[b * R2 + i] = ex_get<i * (N / R2), C>(ex, base);
+      });
+    }
     ex.sync();
     run_stages<N, E, SIGN, NS * R, Rest...>(v, j, tw, tws, ex);
   }
@@ -207,6 +270,10 @@ struct ColEx {
   int slot;
   __device__ __forceinline__ void put(int e, C v) { s[e * SLOTS + slot] = v; }
   __device__ __forceinline__ C get(int e) const { return s[e * SLOTS + slot]; }
+  template <int OFF>
+  __device__ __forceinline__ void put2(int base, C v) { (s + slot + base * SLOTS)[OFF * SLOTS] = v; }
+  template <int OFF>
+  __device__ __forceinline__ C get2(int base) const { return (s + slot + base * SLOTS)[OFF * SLOTS]; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 
@@ -222,22 +289,39 @@ struct ColExPad {
   __device__ __forceinline__ static int row(int e) { return e + (e >> 4); }
   __device__ __forceinline__ void put(int e, C v) { s[row(e) * SLOTS + slot] = v; }
   __device__ __forceinline__ C get(int e) const { return s[row(e) * SLOTS + slot]; }
+  // row(base + OFF) = row(base) + row(OFF) (see RowEx)
+  template <int OFF>
+  __device__ __forceinline__ void put2(int base, C v) { (s + slot + row(base) * SLOTS)[row(OFF) * SLOTS] = v; }
+  template <int OFF>
+  __device__ __forceinline__ C get2(int base) const { return (s + slot + row(base) * SLOTS)[row(OFF) * SLOTS]; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 constexpr int colx_rows(int n) { return n + n / 16; }
 
 // Row exchange: row-contiguous, one pad element per 128 B (spreads the
-// stride-R writes of the first stage across banks).
-template <typename C>
+// stride-R writes of the first stage across banks). For the power-of-two
+// stages here pad(base + off) = pad(base) + pad(off): a stage writes element
+// base + i NS with base = (jj/NS) NS R + jj%NS, and base mod PER plus
+// (i NS) mod PER never reaches PER (PER | NS, or NS R | PER, or NS < PER <= NS R
+// with base mod PER = jj%NS); reads take jj + i N/R2 with jj < N/R2 likewise.
+// ALL: every team of the block owns a row (no predication).
+template <typename C, bool ALL = false>
 struct RowEx {
   C* s;
   bool active = true;  // idle teams (beyond the tile's rows) keep to the barriers only
   static constexpr int PER = 128 / (int)sizeof(C);
-  __device__ __forceinline__ static int pad(int e) { return e + e / PER; }
+  __host__ __device__ __forceinline__ static constexpr int pad(int e) { return e + e / PER; }
+  __device__ __forceinline__ bool on() const { return ALL || active; }
   __device__ __forceinline__ void put(int e, C v) {
-    if (active) s[pad(e)] = v;
+    if (on()) s[pad(e)] = v;
   }
-  __device__ __forceinline__ C get(int e) const { return active ? s[pad(e)] : C{}; }
+  __device__ __forceinline__ C get(int e) const { return on() ? s[pad(e)] : C{}; }
+  template <int OFF>
+  __device__ __forceinline__ void put2(int base, C v) {
+    if (on()) (s + pad(base))[pad(OFF)] = v;
+  }
+  template <int OFF>
+  __device__ __forceinline__ C get2(int base) const { return on() ? (s + pad(base))[pad(OFF)] : C{}; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 
@@ -254,6 +338,7 @@ struct F2Params {
   uint64_t uh;  // ceil(U/2): noise units per half Philox (grfc_internal.cuh unit_pair)
   // fp32 copies for the SFU density path
   float f_wstep1, f_wstep2, f_sqrt_c, f_ell2, f_nhalf_alpha, f_gauss_k, f_scale;
+  float f_lg2K;  // log2(sqrt_c * scale / sqrt 2) for the folded Matern multiplier
   int family;
   DensityDesc D;
   GridDesc g;
@@ -340,6 +425,15 @@ template <typename T, typename C>
 __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
   if (packed) return mk<C>(X.x + X.y, X.x - X.y);
   if (mid) return mk<C>((T)2 * X.x, (T)-2 * X.y);
+#ifndef GRFC_EPI2
+#define GRFC_EPI2 1
+#endif
+  if constexpr (GRFC_EPI2 && sizeof(T) == 4) {
+    // packed fp32x2: s = X + conj P, d = X - conj P, Z = s + i (w d)
+    const unsigned long long x = f2pk(X.x, X.y), pc = f2pk(P.x, -P.y);
+    const float2 t = cmul(w, f2upk(f2sub(x, pc)));
+    return f2upk(f2add(f2add(x, pc), f2pk(-t.y, t.x)));
+  }
   const C s = mk<C>(X.x + P.x, X.y - P.y);
   const C d = mk<C>(X.x - P.x, X.y + P.y);
   const C t = cmul(w, d);
@@ -397,13 +491,17 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll 2
     for (int t = 0; t < E / 2; ++t) {
       const int k1 = j + t * TT;
-      float a0, b0, a1, b1;
-      unit_quad_f32(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col), a0, b0, a1, b1);
+      const uint4 r = philox_draw(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col));
+      float rad0, s0, c0, rad1, s1, c1;
+      box_muller_parts_f32(r.x, r.y, rad0, s0, c0);
+      box_muller_parts_f32(r.z, r.w, rad1, s1, c1);
       const float q0 = rowq[k1], q1 = rowq[k1 + N1 / 2];
-      const float m0 = matern ? K * ex2_approx(p.f_nhalf_alpha * lg2_approx(A + q0)) : B * q0;
-      const float m1 = matern ? K * ex2_approx(p.f_nhalf_alpha * lg2_approx(A + q1)) : B * q1;
-      sm[k1 * SLOTS + slot] = mk<C>((T)(a0 * m0), (T)(-b0 * m0));
-      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(a1 * m1), (T)(-b1 * m1));
+      // Matern: K ex2(-alpha/2 lg2(A + q)) with K folded into the exponent (lg2 K)
+      const float m0 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q0), p.f_lg2K)) : B * q0;
+      const float m1 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q1), p.f_lg2K)) : B * q1;
+      const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
+      sm[k1 * SLOTS + slot] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
     }
   } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
     const T r = (T)0.70710678118654752440, sc = (T)p.scale;
@@ -488,7 +586,7 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 
 // Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
 // real field rows out. Block = RPT * (M/E) threads.
-template <typename T, int M, int RPT>
+template <typename T, int M, int RPT, int NT = 0>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
                                          const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
                                          uint32_t* sig = nullptr) {
@@ -508,7 +606,9 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcg(&Wr[j + b * TT + i * (M / R0)]);
   // Release of the CTA's previous tile; its fence overlaps the W loads' latency.
   if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
-  RowEx<C> ex{reinterpret_cast<C*>(smem_raw) + (rl < RPT ? rl : 0) * row_pitch<M, C>(), rl < RPT};
+  // every team owns a row when the block holds exactly RPT teams (c2: 16 x 16 threads)
+  constexpr bool ALL = NT == RPT * TT;
+  RowEx<C, ALL> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(), ALL || rl < RPT};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   C* o = reinterpret_cast<C*>(of + (int64_t)row * (2 * M));
@@ -556,7 +656,19 @@ struct F2Sched {
   uint32_t F, L, S, strips, rtiles;
   // GRFC_TILE_STATS=1: per-launch cycle counters [col, row, col-wait, row-wait, ticket, ncol, nrow]
   unsigned long long* stats;
+  // f / S = umulhi(f, s_magic) when s_magic != 0 (host-checked: F * S < 2^32)
+  uint32_t s_magic;
 };
+
+// Ring-slot division of the tile decoder (thread 0, once per tile).
+__device__ __forceinline__ void slot_of(const F2Sched& q, uint32_t f, uint32_t& slot, uint32_t& use) {
+  use = q.s_magic ? __umulhi(f, q.s_magic) : f / q.S;
+  slot = f - use * q.S;
+}
+inline uint32_t slot_magic(uint32_t F, uint32_t S) {
+  // floor(f / S) = floor(f * (floor(2^32 / S) + 1) / 2^32) whenever f * S < 2^32
+  return (uint64_t)F * S < (1ull << 32) ? (uint32_t)((1ull << 32) / S + 1) : 0u;
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -584,6 +696,9 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 // tuned for the c2 shape (fp32 512 columns: 4 x 256 threads at 64 registers,
 // no spills; 3 CTAs at 80 registers measured 2% slower); other shapes let
 // ptxas choose.
+#ifndef GRFC_TILE_STATS_BUILD
+#define GRFC_TILE_STATS_BUILD 0
+#endif
 #ifndef GRFC_FUSED_MINB
 #define GRFC_FUSED_MINB 4
 #endif
@@ -610,7 +725,10 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   // Thread 0 signals tile i's completion after that barrier; only if i+1's
   // dependency was not yet met does it spin and add a second barrier.
   const uint64_t slot_elems = (uint64_t)N1 * M;
-  const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
+  // tiles per field are compile-time (strips = M / 2CB, row tiles = N1 / RPT): the
+  // decoder's divisions by them are shifts; the ring-slot division is a multiply-high
+  constexpr uint32_t STRIPS = M / (2 * ColPlan<N1, T>::X), RT = N1 / RPT, G = STRIPS + RT;
+  const uint32_t pro = q.L * STRIPS, nfull = q.F - q.L;
   const uint32_t total = q.F * G;
   struct Tile {
     bool col;
@@ -620,27 +738,26 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     Tile x;
     if (t < pro) {
       x.col = true;
-      x.f = t / q.strips;
-      x.idx = t % q.strips;
+      x.f = t / STRIPS;
+      x.idx = t % STRIPS;
     } else if ((t -= pro) < nfull * G) {
       const uint32_t g = t / G, r = t % G;
-      x.col = r < q.strips;
+      x.col = r < STRIPS;
       x.f = x.col ? g + q.L : g;
-      x.idx = x.col ? r : r - q.strips;
+      x.idx = x.col ? r : r - STRIPS;
     } else {
       t -= nfull * G;
       x.col = false;
-      x.f = nfull + t / q.rtiles;
-      x.idx = t % q.rtiles;
+      x.f = nfull + t / RT;
+      x.idx = t % RT;
     }
-    x.slot = x.f % q.S;
-    x.use = x.f / q.S;
+    slot_of(q, x.f, x.slot, x.use);
     return x;
   };
   // dependency counter / target of a tile (target 0: none)
   auto dep_of = [&](const Tile& x, const uint32_t*& ctr) -> uint32_t {
     ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
-    return x.col ? x.use * q.rtiles : (x.use + 1) * q.strips;
+    return x.col ? x.use * RT : (x.use + 1) * STRIPS;
   };
   // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
   // after, its atomic in flight). At the start of each tile it issues a
@@ -691,9 +808,11 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   }
   __syncthreads();
   uint32_t* done_ctr = nullptr;  // thread 0: counter of the tile just finished
+  // tile timing counters are compiled in only with -DGRFC_TILE_STATS_BUILD=1
+  const bool STATS = GRFC_TILE_STATS_BUILD && q.stats;
   long long c_col = 0, c_row = 0, c_wc = 0, c_wr = 0, c_tk = 0, n_col = 0, n_row = 0;
   for (;;) {
-    long long t0 = q.stats ? clock64() : 0;
+    long long t0 = STATS ? clock64() : 0;
     const Msg m = s_msg;
     if (threadIdx.x == 0) {
       if (tA < total) {  // early dependency load of the next tile
@@ -722,8 +841,8 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
       }
       __syncthreads();
     }
-    if (q.stats) (m.col ? c_wc : c_wr) += clock64() - t0;
-    long long b = q.stats ? clock64() : 0;
+    if (STATS) (m.col ? c_wc : c_wr) += clock64() - t0;
+    long long b = STATS ? clock64() : 0;
     C_t<T>* Wf = ring + m.slot * slot_elems;
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
@@ -731,25 +850,26 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
                            nullptr, 0, done_ctr);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
+                                                     smem_raw, done_ctr);
       done_ctr = &q.row_done[m.slot];
     }
     // every tile has internal barriers, so all threads have read s_msg
-    long long e = q.stats ? clock64() : 0;
+    long long e = STATS ? clock64() : 0;
     if (threadIdx.x == 0) {
       publish(tA, dep_v, tB);
       tA = tB;
       tB = tB < total ? claim() : total;
     }
     __syncthreads();
-    if (q.stats) {
+    if (STATS) {
       (m.col ? c_col : c_row) += e - b;
       c_tk += clock64() - e;
       ++(m.col ? n_col : n_row);
     }
   }
   if (threadIdx.x == 0 && done_ctr) red_release_add(done_ctr, 1u);  // the CTA's last tile
-  if (q.stats && threadIdx.x == 0) {
+  if (STATS && threadIdx.x == 0) {
     atomicAdd(&q.stats[0], (unsigned long long)c_col);
     atomicAdd(&q.stats[1], (unsigned long long)c_row);
     atomicAdd(&q.stats[2], (unsigned long long)c_wc);
@@ -785,7 +905,7 @@ __global__ void __launch_bounds__(row_threads<M, T>())
   constexpr int RPB = RowPlan<M, T>::X;
   const int64_t r0 = (int64_t)blockIdx.x * RPB;
   const int64_t f = r0 / rows_per_field;
-  row_tile<T, M, RPB>(W + f * (int64_t)rows_per_field * M, (int)(r0 - f * rows_per_field), rows_per_field,
+  row_tile<T, M, RPB, row_threads<M, T>()>(W + f * (int64_t)rows_per_field * M, (int)(r0 - f * rows_per_field), rows_per_field,
                       out + f * out_stride, tw2, smem_raw);
 }
 
@@ -811,6 +931,7 @@ inline F2Params make_params(const Fast2D& f) {
   p.f_nhalf_alpha = (float)(-0.5 * p.alpha);
   p.f_gauss_k = (float)(-0.25 * p.ell * p.ell * 1.4426950408889634);  // -ell^2/4 * log2(e)
   p.f_scale = (float)p.scale;
+  p.f_lg2K = (float)std::log2(p.sqrt_c * p.scale * 0.70710678118654752440);
   p.D = f.D;
   p.g = f.g;
   return p;
@@ -886,6 +1007,7 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   q.F = (uint32_t)nf;
   q.strips = (uint32_t)f.strips;
   q.rtiles = (uint32_t)f.rtiles;
+  q.s_magic = slot_magic(q.F, q.S);
   uint32_t* ctr = (uint32_t*)ws;  // [ticket][col_done S][row_done S] | ring
   q.ticket = ctr;
   q.col_done = ctr + 1;

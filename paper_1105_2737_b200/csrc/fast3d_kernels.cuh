@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(col_threads<N1, T>())
       signal_done(&q.col_done[slot]);
     } else {
       wait_geq(&q.col_done[slot], (use + 1) * q.strips);
-      row_tile<T, M, RPT>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw);
       signal_done(&q.row_done[slot]);
     }
   }

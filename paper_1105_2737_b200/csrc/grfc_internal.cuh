@@ -175,13 +175,20 @@ __device__ __forceinline__ void sincos_approx(float x, float& s, float& c) {
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(x));
 }
 
+// fp32 Box-Muller in parts: z0 = rad c, z1 = rad s. u1 = ((x >> 8) + 1) 2^-24 in
+// (0, 1], u2 = (y >> 8) 2^-24 in [0, 1), angle 2 pi u2 - pi; the 2^-24 of u2 is
+// folded into the angle's FMA constant (exact: the product is the same real
+// number, so the result is bit-identical to fma(u2, 2 pi, -pi)).
+__device__ __forceinline__ void box_muller_parts_f32(uint32_t x, uint32_t y, float& rad, float& s, float& c) {
+  const float u1 = (float)((x >> 8) + 1u) * 0x1.0p-24f;
+  rad = sqrt_approx(-1.38629436111989061883f * lg2_approx(u1));  // sqrt(-2 ln u1)
+  sincos_approx(__fmaf_rn((float)(y >> 8), 6.28318530717958647693f * 0x1.0p-24f, -3.14159265358979323846f), s, c);
+}
+
 template <>
 __device__ __forceinline__ void box_muller<float>(uint4 r, float& z0, float& z1) {
-  const float u1 = (float)((r.x >> 8) + 1u) * 0x1.0p-24f;  // (0, 1]
-  const float u2 = (float)(r.y >> 8) * 0x1.0p-24f;         // [0, 1)
-  const float rad = sqrt_approx(-1.38629436111989061883f * lg2_approx(u1));  // sqrt(-2 ln u1)
-  float s, c;
-  sincos_approx(6.28318530717958647693f * u2 - 3.14159265358979323846f, s, c);
+  float rad, s, c;
+  box_muller_parts_f32(r.x, r.y, rad, s, c);
   z0 = rad * c;
   z1 = rad * s;
 }
