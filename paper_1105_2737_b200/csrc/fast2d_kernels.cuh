@@ -264,17 +264,43 @@ __device__ __forceinline__ void line_fft(C* v, int j, const C* __restrict__ tw, 
 
 // Column-strip exchange: smem[e * SLOTS + slot]; slots are adjacent lanes,
 // so every access is a full 128 B (fp32) / 256 B (fp64) row: conflict-free.
+// Deferred ring-slot dependency of a column tile, checked by thread 0 at the
+// exchange barriers (the tile writes W only after its last exchange): `seen`
+// is the counter value thread 0 loaded when the tile started, so the common
+// case costs one compare and no extra barrier.
+// `skip` barriers pass before the check (the last exchange barrier checks).
+struct LateDep {
+  const uint32_t* ctr = nullptr;
+  uint32_t target = 0, seen = 0;
+  int skip = 0;
+  __device__ __forceinline__ void check() {
+    if (ctr && threadIdx.x == 0 && skip-- <= 0 && seen < target) {
+      while ((seen = *(const volatile uint32_t*)ctr) < target) __nanosleep(128);
+    }
+  }
+};
+template <typename RS>
+struct RCount;
+template <int... Rs>
+struct RCount<Radices<Rs...>> {
+  static constexpr int value = sizeof...(Rs);
+};
+
 template <typename C, int SLOTS>
 struct ColEx {
   C* s;
   int slot;
+  LateDep dep{};
   __device__ __forceinline__ void put(int e, C v) { s[e * SLOTS + slot] = v; }
   __device__ __forceinline__ C get(int e) const { return s[e * SLOTS + slot]; }
   template <int OFF>
   __device__ __forceinline__ void put2(int base, C v) { (s + slot + base * SLOTS)[OFF * SLOTS] = v; }
   template <int OFF>
   __device__ __forceinline__ C get2(int base) const { return (s + slot + base * SLOTS)[OFF * SLOTS]; }
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ void sync() {
+    dep.check();
+    __syncthreads();
+  }
 };
 
 // Column-strip exchange with one padding row-block every 16 rows (row e at
@@ -286,6 +312,7 @@ template <typename C, int SLOTS>
 struct ColExPad {
   C* s;
   int slot;
+  LateDep dep{};
   __device__ __forceinline__ static int row(int e) { return e + (e >> 4); }
   __device__ __forceinline__ void put(int e, C v) { s[row(e) * SLOTS + slot] = v; }
   __device__ __forceinline__ C get(int e) const { return s[row(e) * SLOTS + slot]; }
@@ -294,7 +321,10 @@ struct ColExPad {
   __device__ __forceinline__ void put2(int base, C v) { (s + slot + row(base) * SLOTS)[row(OFF) * SLOTS] = v; }
   template <int OFF>
   __device__ __forceinline__ C get2(int base) const { return (s + slot + row(base) * SLOTS)[row(OFF) * SLOTS]; }
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ void sync() {
+    dep.check();
+    __syncthreads();
+  }
 };
 constexpr int colx_rows(int n) { return n + n / 16; }
 
@@ -440,6 +470,9 @@ __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
   return mk<C>(s.x - t.y, s.y + t.x);
 }
 
+#ifndef GRFC_EARLY_REL
+#define GRFC_EARLY_REL 1
+#endif
 // ---------------------------------------------------------------- tiles
 // Release-increment of a completion counter: orders this thread's (and, after
 // a CTA barrier, the CTA's) prior writes before the increment. Emits
@@ -457,7 +490,7 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 
 // Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
 // generation fused in front and the Z epilogue behind. Block = col_threads.
-template <typename T, int N1, int ALG>
+template <typename T, int N1, int ALG, int MC = 0>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
@@ -478,6 +511,9 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // it is only needed before the W stores, so its latency hides behind the tile.
   uint32_t dep_seen = 0;
   if (dep && threadIdx.x == 0) dep_seen = ld_relaxed_u32(dep);
+  // GRFC_EARLY_REL: release the previous tile before generation (its consumers
+  // wait on it; the fence stalls warp 0 only while the others generate)
+  if (GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
   if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one
     // Philox call. sqrt(g) from the per-CTA row table rowq (fused2d_row_table):
@@ -529,7 +565,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   __syncthreads();
   // Release of the CTA's previous tile: no global stores are in flight here,
   // so the fence in front of the increment is cheap (persistent kernel).
-  if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
+  if (!GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
   C v[E];
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
@@ -540,16 +576,22 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // at SLOTS = 8 the extra index arithmetic costs more than the 2-way conflicts
   using Ex = std::conditional_t<(SLOTS <= 4), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
   Ex ex{sm, slot};
+  // The slot's previous field must be consumed before W is overwritten: checked
+  // at the FFT's exchange barriers (all W stores follow the last one).
+  constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
+  if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
-
-  // The slot's previous field must be consumed before W is overwritten.
-  if (dep) {
+  if (dep && !has_ex) {
     if (threadIdx.x == 0 && dep_seen < dep_target)
       while (ld_relaxed_u32(dep) < dep_target) __nanosleep(256);
     __syncthreads();
   }
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
   const bool special = packed || mid;
+  // one 64-bit pointer per thread; with a compile-time M (persistent kernel) every
+  // store is that pointer plus an immediate
+  const int64_t mstride = MC > 0 ? (int64_t)MC : (int64_t)p.m;
+  C* __restrict__ wp = Wf + (int64_t)j * mstride + col;
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -558,8 +600,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       C P;
       P.x = __shfl_xor_sync(0xffffffffu, v[e].x, CB);
       P.y = __shfl_xor_sync(0xffffffffu, v[e].y, CB);
-      const int row = j + b * TT + i * (N1 / RL);
-      if (!special) __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], P, false, false, w));
+      const int rr = b * TT + i * (N1 / RL);
+      if (!special) __stcg(wp + rr * mstride, epilogue_z<T>(v[e], P, false, false, w));
     }
   if (special) {
 #pragma unroll
@@ -567,8 +609,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll
       for (int i = 0; i < RL; ++i) {
         const int e = b * RL + i;
-        const int row = j + b * TT + i * (N1 / RL);
-        __stcg(&Wf[(int64_t)row * p.m + col], epilogue_z<T>(v[e], v[e], packed, mid, w));
+        const int rr = b * TT + i * (N1 / RL);
+        __stcg(wp + rr * mstride, epilogue_z<T>(v[e], v[e], packed, mid, w));
       }
   }
 }
@@ -696,6 +738,12 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 // tuned for the c2 shape (fp32 512 columns: 4 x 256 threads at 64 registers,
 // no spills; 3 CTAs at 80 registers measured 2% slower); other shapes let
 // ptxas choose.
+#ifndef GRFC_RES1
+#define GRFC_RES1 1
+#endif
+#ifndef GRFC_COL_LATE_WAIT
+#define GRFC_COL_LATE_WAIT 1
+#endif
 #ifndef GRFC_TILE_STATS_BUILD
 #define GRFC_TILE_STATS_BUILD 0
 #endif
@@ -755,9 +803,11 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     return x;
   };
   // dependency counter / target of a tile (target 0: none)
+  // Column tiles check their ring-slot dependency late (before their W stores,
+  // see col_tile), so only row tiles wait up front.
   auto dep_of = [&](const Tile& x, const uint32_t*& ctr) -> uint32_t {
     ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
-    return x.col ? x.use * RT : (x.use + 1) * STRIPS;
+    return x.col ? (GRFC_COL_LATE_WAIT ? 0u : x.use * RT) : (x.use + 1) * STRIPS;
   };
   // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
   // after, its atomic in flight). At the start of each tile it issues a
@@ -768,7 +818,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   // Thread 0 also decodes the tiles (integer divisions) and publishes them in
   // shared memory, so the other threads only read the message.
   struct Msg {
-    uint32_t t, ready, col, f, idx, slot, pf;
+    uint32_t t, ready, col, f, idx, slot, use, pf;
     uint64_t pf_off;  // element offset of the W rows of the tile after next (pf: it is a row tile)
   };
   __shared__ Msg s_msg;
@@ -782,15 +832,21 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     m.ready = 1;
     if (t < total) {
       const Tile x = decode(t);
-      m.col = x.col, m.f = x.f, m.idx = x.idx, m.slot = x.slot;
+      m.col = x.col, m.f = x.f, m.idx = x.idx, m.slot = x.slot, m.use = x.use;
       const uint32_t* ctr;
       const uint32_t target = dep_of(x, ctr);
       if (target) {
-        if (v < target) v = ld_relaxed_u32(ctr);
-        m.ready = v >= target;
-        // rows read what other CTAs wrote: acquire; a column tile's ring-slot reuse
-        // (write after the rows' reads) needs no L1-invalidating acquire
-        if (m.ready && !x.col) (void)ld_acquire_u32(ctr);
+        if (GRFC_RES1 && !x.col) {
+          // one round trip: the acquire load both checks and orders
+          v = ld_acquire_u32(ctr);
+          m.ready = v >= target;
+        } else {
+          if (v < target) v = ld_relaxed_u32(ctr);
+          m.ready = v >= target;
+          // rows read what other CTAs wrote: acquire; a column tile's ring-slot reuse
+          // (write after the rows' reads) needs no L1-invalidating acquire
+          if (m.ready && !x.col) (void)ld_acquire_u32(ctr);
+        }
       }
     }
     if (t2 < total) {
@@ -802,9 +858,13 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   };
   if (threadIdx.x == 0) {
     const uint32_t t0 = claim();
-    tA = claim();
-    tB = claim();
-    publish(t0, 0, tA);
+    if (GRFC_RES1) {
+      publish(t0, 0, total);
+    } else {
+      tA = claim();
+      tB = claim();
+      publish(t0, 0, tA);
+    }
   }
   __syncthreads();
   uint32_t* done_ctr = nullptr;  // thread 0: counter of the tile just finished
@@ -815,7 +875,11 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     long long t0 = STATS ? clock64() : 0;
     const Msg m = s_msg;
     if (threadIdx.x == 0) {
-      if (tA < total) {  // early dependency load of the next tile
+      if (GRFC_RES1) {
+        // GRFC_RES1: one reservation — the next tile's ticket is claimed now and
+        // read at the end of this tile (its round trip hides behind the tile)
+        if (m.t < total) tA = claim();
+      } else if (tA < total) {  // early dependency load of the next tile
         const uint32_t* ctr;
         dep_of(decode(tA), ctr);
         dep_v = ld_relaxed_u32(ctr);
@@ -846,8 +910,8 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     C_t<T>* Wf = ring + m.slot * slot_elems;
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
-      col_tile<T, N1, ALG>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
-                           nullptr, 0, done_ctr);
+      col_tile<T, N1, ALG, M>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
+                              GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr);
       done_ctr = &q.col_done[m.slot];
     } else {
       row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
@@ -857,9 +921,13 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     // every tile has internal barriers, so all threads have read s_msg
     long long e = STATS ? clock64() : 0;
     if (threadIdx.x == 0) {
-      publish(tA, dep_v, tB);
-      tA = tB;
-      tB = tB < total ? claim() : total;
+      if (GRFC_RES1) {
+        publish(tA < total ? tA : total, 0, total);
+      } else {
+        publish(tA, dep_v, tB);
+        tA = tB;
+        tB = tB < total ? claim() : total;
+      }
     }
     __syncthreads();
     if (STATS) {
