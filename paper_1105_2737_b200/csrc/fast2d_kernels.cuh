@@ -190,6 +190,9 @@ __device__ __forceinline__ int stage_in_index(int j, int b, int i) {
 // pad(base + off) = pad(base) + pad(off) for every stage: see RowEx).
 template <typename Ex, typename = void>
 struct HasPut2 : std::false_type {};
+#ifndef GRFC_ROW_WARPSYNC
+#define GRFC_ROW_WARPSYNC 1
+#endif
 #ifndef GRFC_EX2
 #define GRFC_EX2 1
 #endif
@@ -335,7 +338,9 @@ constexpr int colx_rows(int n) { return n + n / 16; }
 // (i NS) mod PER never reaches PER (PER | NS, or NS R | PER, or NS < PER <= NS R
 // with base mod PER = jj%NS); reads take jj + i N/R2 with jj < N/R2 likewise.
 // ALL: every team of the block owns a row (no predication).
-template <typename C, bool ALL = false>
+// WARP: the team of a row lies inside one warp (M/E <= 32 threads), so its
+// exchange needs only __syncwarp, never a CTA barrier.
+template <typename C, bool ALL = false, bool WARP = false>
 struct RowEx {
   C* s;
   bool active = true;  // idle teams (beyond the tile's rows) keep to the barriers only
@@ -352,7 +357,12 @@ struct RowEx {
   }
   template <int OFF>
   __device__ __forceinline__ C get2(int base) const { return on() ? (s + pad(base))[pad(OFF)] : C{}; }
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ void sync() const {
+    if constexpr (WARP)
+      __syncwarp();
+    else
+      __syncthreads();
+  }
 };
 
 template <int N, typename C>
@@ -490,12 +500,19 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 
 // Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
 // generation fused in front and the Z epilogue behind. Block = col_threads.
-template <typename T, int N1, int ALG, int MC = 0>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `hook` runs on thread 0 once per tile, mid-tile (after the generation barrier
+// of a column tile, behind the W loads of a row tile): the persistent
+// scheduler checks the next tile's dependency there, off the critical path.
+template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
                                          const uint32_t* dep = nullptr, uint32_t dep_target = 0,
-                                         uint32_t* sig = nullptr) {
+                                         uint32_t* sig = nullptr, Hook hook = Hook{}) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -566,6 +583,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // Release of the CTA's previous tile: no global stores are in flight here,
   // so the fence in front of the increment is cheap (persistent kernel).
   if (!GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
+  if (threadIdx.x == 0) hook();
   C v[E];
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
@@ -592,6 +610,21 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // store is that pointer plus an immediate
   const int64_t mstride = MC > 0 ? (int64_t)MC : (int64_t)p.m;
   C* __restrict__ wp = Wf + (int64_t)j * mstride + col;
+  // Only the warps of strip 0 hold the packed (0, M) and middle (M/2) columns:
+  // the others take a branch-free path (warp-uniform test).
+  if (!__any_sync(0xffffffffu, special)) {
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) {
+        const int e = b * RL + i;
+        C P;
+        P.x = __shfl_xor_sync(0xffffffffu, v[e].x, CB);
+        P.y = __shfl_xor_sync(0xffffffffu, v[e].y, CB);
+        __stcg(wp + (b * TT + i * (N1 / RL)) * mstride, epilogue_z<T>(v[e], P, false, false, w));
+      }
+    return;
+  }
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -628,10 +661,10 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 
 // Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
 // real field rows out. Block = RPT * (M/E) threads.
-template <typename T, int M, int RPT, int NT = 0>
+template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
                                          const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
-                                         uint32_t* sig = nullptr) {
+                                         uint32_t* sig = nullptr, Hook hook = Hook{}) {
   using C = C_t<T>;
   using PL = RowPlan<M, T>;
   constexpr int E = PL::E, TT = M / E;
@@ -648,9 +681,11 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcg(&Wr[j + b * TT + i * (M / R0)]);
   // Release of the CTA's previous tile; its fence overlaps the W loads' latency.
   if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
+  if (threadIdx.x == 0) hook();
   // every team owns a row when the block holds exactly RPT teams (c2: 16 x 16 threads)
   constexpr bool ALL = NT == RPT * TT;
-  RowEx<C, ALL> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(), ALL || rl < RPT};
+  constexpr bool WARP = GRFC_ROW_WARPSYNC && TT <= 32 && 32 % TT == 0;
+  RowEx<C, ALL, WARP> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(), ALL || rl < RPT};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   C* o = reinterpret_cast<C*>(of + (int64_t)row * (2 * M));
@@ -738,6 +773,9 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 // tuned for the c2 shape (fp32 512 columns: 4 x 256 threads at 64 registers,
 // no spills; 3 CTAs at 80 registers measured 2% slower); other shapes let
 // ptxas choose.
+#ifndef GRFC_MID_CHECK
+#define GRFC_MID_CHECK 1
+#endif
 #ifndef GRFC_RES1
 #define GRFC_RES1 1
 #endif
@@ -837,9 +875,10 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
       const uint32_t target = dep_of(x, ctr);
       if (target) {
         if (GRFC_RES1 && !x.col) {
-          // one round trip: the acquire load both checks and orders
-          v = ld_acquire_u32(ctr);
-          m.ready = v >= target;
+          // v = 1 + the value acquired mid-tile (0: none); else one round trip here,
+          // the acquire load both checking and ordering
+          m.ready = v > target;
+          if (!m.ready) m.ready = ld_acquire_u32(ctr) >= target;
         } else {
           if (v < target) v = ld_relaxed_u32(ctr);
           m.ready = v >= target;
@@ -908,21 +947,34 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     if (STATS) (m.col ? c_wc : c_wr) += clock64() - t0;
     long long b = STATS ? clock64() : 0;
     C_t<T>* Wf = ring + m.slot * slot_elems;
+    // GRFC_RES1 mid-tile check (thread 0): the next ticket's atomic, issued at the
+    // top of this tile, has returned; if it is a row tile, its dependency counter
+    // is read now with acquire semantics (ordering the CTA's later W reads after
+    // the producers' releases), so publish() needs no round trip when it is met.
+    auto hook = [&]() {
+      if (GRFC_RES1 && GRFC_MID_CHECK && tA < total) {
+        const Tile y = decode(tA);
+        const uint32_t* ctr;
+        if (!y.col && dep_of(y, ctr)) dep_v = ld_acquire_u32(ctr) + 1u;  // +1: "acquired" marker
+      }
+    };
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
       col_tile<T, N1, ALG, M>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
-                              GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr);
+                              GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr,
+                              hook);
       done_ctr = &q.col_done[m.slot];
     } else {
       row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
-                                                     smem_raw, done_ctr);
+                                                     smem_raw, done_ctr, hook);
       done_ctr = &q.row_done[m.slot];
     }
     // every tile has internal barriers, so all threads have read s_msg
     long long e = STATS ? clock64() : 0;
     if (threadIdx.x == 0) {
       if (GRFC_RES1) {
-        publish(tA < total ? tA : total, 0, total);
+        publish(tA < total ? tA : total, dep_v, total);
+        dep_v = 0;
       } else {
         publish(tA, dep_v, tB);
         tA = tB;
