@@ -190,6 +190,9 @@ __device__ __forceinline__ int stage_in_index(int j, int b, int i) {
 // pad(base + off) = pad(base) + pad(off) for every stage: see RowEx).
 template <typename Ex, typename = void>
 struct HasPut2 : std::false_type {};
+#ifndef GRFC_GEN_NOBAR
+#define GRFC_GEN_NOBAR 1
+#endif
 #ifndef GRFC_ROW_WARPSYNC
 #define GRFC_ROW_WARPSYNC 1
 #endif
@@ -579,7 +582,10 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       sm[k1 * SLOTS + slot] = x;
     }
   }
-  __syncthreads();
+  // Every thread reads back exactly the rows it generated (rows j + u TT, the
+  // stage-0 inputs of its team position), so no CTA barrier is needed here;
+  // the one below orders these reads before the first exchange's writes.
+  if (!GRFC_GEN_NOBAR) __syncthreads();
   // Release of the CTA's previous tile: no global stores are in flight here,
   // so the fence in front of the increment is cheap (persistent kernel).
   if (!GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
