@@ -68,7 +68,9 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
 #pragma unroll
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[rs * PITCH + RowEx<C>::pad(j + b * TT + i * (M / R0))];
   __syncthreads();
-  RowEx<C> ex{sm + rs * PITCH, live};
+  // the row's team is a half warp: warp-level exchange (as row_tile)
+  constexpr bool WARP = GRFC_ROW_WARPSYNC && TT <= 32 && 32 % TT == 0;
+  RowEx<C, false, WARP> ex{sm + rs * PITCH, live};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   const int row = rl < H ? r0 + rl : r0 + (rl - H) + N1 / 2;
@@ -127,61 +129,67 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
     }
   __syncthreads();
   ColEx<C, SLOTS> ex{sm, slot};
-  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
-  // 3. U -> smem in natural row order
-#pragma unroll
-  for (int b = 0; b < E / RL; ++b)
-#pragma unroll
-    for (int i = 0; i < RL; ++i) sm[(j + b * TT + i * (N1 / RL)) * SLOTS + slot] = v[b * RL + i];
-  __syncthreads();
-  // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col).
-  // fp32 Matern / Gaussian interior columns: sqrt(g) from the per-CTA row table
-  // (fused2d_row_table; rowq is even in k1, so row -k1 reuses rowq[k1]) and the
-  // two columns' factors, as Algorithm 2's col_tile does.
-  const T sc = (T)p.scale;
-  const bool fast_dens = sizeof(T) == 4 && rowq && !packed;
-  float Ac = 0.f, Ap = 0.f, Bc = 0.f, Bp = 0.f;
-  const bool matern = p.family == GRFC_DENSITY_MATERN;
-  if (fast_dens) {
-    const int pc = mid ? col : pcol;
-    const float wc = (float)(col <= p.n2 / 2 ? col : col - p.n2) * p.f_wstep2;
-    const float wp = (float)(pc <= p.n2 / 2 ? pc : pc - p.n2) * p.f_wstep2;
-    Ac = 1.0f + p.f_ell2 * wc * wc;
-    Ap = 1.0f + p.f_ell2 * wp * wp;
-    Bc = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wc * wc);
-    Bp = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wp * wp);
-  }
-  const float Km = p.f_sqrt_c * p.f_scale;
-#pragma unroll
-  for (int b = 0; b < E / R0; ++b)
-#pragma unroll
-    for (int i = 0; i < R0; ++i) {
-      const int k1 = j + b * TT + i * (N1 / R0), km = (N1 - k1) & (N1 - 1);
-      C Vk, Vm;
-      if (packed) {
-        const C Uk = sm[k1 * SLOTS + slot], Um = sm[km * SLOTS + slot];
-        // F0(k1) = (U(k1) + conj U(-k1))/2 ; FM(-k1) = -i (U(-k1) - conj U(k1))/2
-        const C F0k = mk<C>((Uk.x + Um.x) * half, (Uk.y - Um.y) * half);
-        const C FMm = mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half);
-        Vk = cscale(F0k, sqrt_g2<T>(p, k1, 0) * sc);
-        Vm = cscale(FMm, sqrt_g2<T>(p, km, p.m) * sc);
-      } else if (fast_dens) {
-        const float q = rowq[k1];
-        const float mk_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ac + q)) : Bc * q;
-        const float mm_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ap + q)) : Bp * q;
-        Vk = cscale(sm[k1 * SLOTS + slot], (T)mk_);
-        Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], (T)mm_);
-      } else {
-        Vk = cscale(sm[k1 * SLOTS + slot], sqrt_g2<T>(p, k1, col) * sc);
-        Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], sqrt_g2<T>(p, km, mid ? col : pcol) * sc);
-      }
-      const C cV = cconj(Vk);
-      const C sum = cadd(cV, Vm), dif = csub(cV, Vm);
-      const C t = cmul(w, dif);
-      v[b * R0 + i] = mk<C>(sum.x - t.y, sum.y + t.x);
+  // Both column FFTs run through ONE copy of the transform code (a rolled
+  // two-pass loop): the kernel's three tile types otherwise overflow the
+  // instruction cache (ncu: "no instruction" stalls).
+#pragma unroll 1
+  for (int pass = 0;; ++pass) {
+    line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    if (pass == 1) break;
+    // 3. U -> smem in natural row order
+  #pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+  #pragma unroll
+      for (int i = 0; i < RL; ++i) sm[(j + b * TT + i * (N1 / RL)) * SLOTS + slot] = v[b * RL + i];
+    __syncthreads();
+    // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col).
+    // fp32 Matern / Gaussian interior columns: sqrt(g) from the per-CTA row table
+    // (fused2d_row_table; rowq is even in k1, so row -k1 reuses rowq[k1]) and the
+    // two columns' factors, as Algorithm 2's col_tile does.
+    const T sc = (T)p.scale;
+    const bool fast_dens = sizeof(T) == 4 && rowq && !packed;
+    float Ac = 0.f, Ap = 0.f, Bc = 0.f, Bp = 0.f;
+    const bool matern = p.family == GRFC_DENSITY_MATERN;
+    if (fast_dens) {
+      const int pc = mid ? col : pcol;
+      const float wc = (float)(col <= p.n2 / 2 ? col : col - p.n2) * p.f_wstep2;
+      const float wp = (float)(pc <= p.n2 / 2 ? pc : pc - p.n2) * p.f_wstep2;
+      Ac = 1.0f + p.f_ell2 * wc * wc;
+      Ap = 1.0f + p.f_ell2 * wp * wp;
+      Bc = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wc * wc);
+      Bp = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wp * wp);
     }
-  __syncthreads();
-  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    const float Km = p.f_sqrt_c * p.f_scale;
+  #pragma unroll
+    for (int b = 0; b < E / R0; ++b)
+  #pragma unroll
+      for (int i = 0; i < R0; ++i) {
+        const int k1 = j + b * TT + i * (N1 / R0), km = (N1 - k1) & (N1 - 1);
+        C Vk, Vm;
+        if (packed) {
+          const C Uk = sm[k1 * SLOTS + slot], Um = sm[km * SLOTS + slot];
+          // F0(k1) = (U(k1) + conj U(-k1))/2 ; FM(-k1) = -i (U(-k1) - conj U(k1))/2
+          const C F0k = mk<C>((Uk.x + Um.x) * half, (Uk.y - Um.y) * half);
+          const C FMm = mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half);
+          Vk = cscale(F0k, sqrt_g2<T>(p, k1, 0) * sc);
+          Vm = cscale(FMm, sqrt_g2<T>(p, km, p.m) * sc);
+        } else if (fast_dens) {
+          const float q = rowq[k1];
+          const float mk_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ac + q)) : Bc * q;
+          const float mm_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ap + q)) : Bp * q;
+          Vk = cscale(sm[k1 * SLOTS + slot], (T)mk_);
+          Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], (T)mm_);
+        } else {
+          Vk = cscale(sm[k1 * SLOTS + slot], sqrt_g2<T>(p, k1, col) * sc);
+          Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], sqrt_g2<T>(p, km, mid ? col : pcol) * sc);
+        }
+        const C cV = cconj(Vk);
+        const C sum = cadd(cV, Vm), dif = csub(cV, Vm);
+        const C t = cmul(w, dif);
+        v[b * R0 + i] = mk<C>(sum.x - t.y, sum.y + t.x);
+      }
+    __syncthreads();
+  }
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -189,10 +197,11 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
 }
 
 #ifndef GRFC_ALG1_MINB
-#define GRFC_ALG1_MINB 3
+#define GRFC_ALG1_MINB 4
 #endif
-// Three resident 256-thread CTAs per SM for the fp32 shapes (<= 80 registers,
-// no spills at 512 x 256: 98 -> 113 Gpts/s vs two); larger blocks / fp64 let ptxas choose.
+// Four resident 256-thread CTAs per SM for the fp32 shapes (64 registers; the few
+// spills cost less than the lost occupancy: 512 x 256 Alg 1 121 -> 125 Gpts/s vs
+// three CTAs at 80 registers, 101 with two); larger blocks / fp64 let ptxas choose.
 template <int N1, int M, typename T>
 constexpr int alg1_min_blocks() {
   return (sizeof(T) == 4 && fused_threads<N1, M, T>() <= 256) ? GRFC_ALG1_MINB : 0;
