@@ -128,7 +128,7 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
       v[b * R0 + i] = X;
     }
   __syncthreads();
-  ColEx<C, SLOTS> ex{sm, slot};
+  std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{sm, slot};
   // Both column FFTs run through ONE copy of the transform code (a rolled
   // two-pass loop): the kernel's three tile types otherwise overflow the
   // instruction cache (ncu: "no instruction" stalls).

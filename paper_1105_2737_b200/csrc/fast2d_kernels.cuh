@@ -333,6 +333,17 @@ struct ColExPad {
   }
 };
 constexpr int colx_rows(int n) { return n + n / 16; }
+// Padded column exchange: with base + immediate addressing (put2/get2) the
+// padding costs no index arithmetic, so every fp32 plan uses it (SLOTS = 8:
+// stage-0 puts 4-way -> 2 wavefronts per warp, the 64-bit minimum); fp64 plans
+// with SLOTS > 4 keep the plain layout.
+#ifndef GRFC_COLPAD
+#define GRFC_COLPAD 1
+#endif
+template <int N1, typename T>
+constexpr bool col_padded() {
+  return ColPlan<N1, T>::X <= 2 || (GRFC_COLPAD && sizeof(T) == 4);
+}
 
 // Row exchange: row-contiguous, one pad element per 128 B (spreads the
 // stride-R writes of the first stage across banks). For the power-of-two
@@ -596,9 +607,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll
     for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[(j + b * TT + i * (N1 / R0)) * SLOTS + slot];
   __syncthreads();
-  // padded exchange only where stage-0 conflicts are 8-way (SLOTS <= 4, N1 = 4096);
-  // at SLOTS = 8 the extra index arithmetic costs more than the 2-way conflicts
-  using Ex = std::conditional_t<(SLOTS <= 4), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
+  using Ex = std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
   Ex ex{sm, slot};
   // The slot's previous field must be consumed before W is overwritten: checked
   // at the FFT's exchange barriers (all W stores follow the last one).
@@ -718,7 +727,7 @@ constexpr int rows_per_tile() {
 template <int N1, int M, typename T>
 constexpr size_t fused_smem() {
   using C = C_t<T>;
-  constexpr size_t a = (size_t)(ColPlan<N1, T>::X <= 2 ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t a = (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
   constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
   return a > b ? a : b;
 }
@@ -1068,7 +1077,7 @@ cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t
                                cudaStream_t s) {
   using C = C_t<T>;
   constexpr int CB = ColPlan<N1, T>::X;
-  const size_t smem = (size_t)(CB <= 2 ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
+  const size_t smem = (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_cols_gen<T, N1, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
