@@ -212,6 +212,9 @@ def kernel_alg_bytes(name, P, H, s):
         "fused_rows_c2r": P * s + P * s,    # read packed spectrum (P/2 complex), write field
         "fused_cols_gen": P * s,            # write packed column-transformed spectrum
         "fused2d_persistent": P * s,        # whole path in one kernel: compulsory field write only
+        "fused2d_alg1_persistent": P * s,   # Algorithm 1, whole path in one kernel
+        "fused3d_colgen": P * s,            # 3D pass A: generation + axis-0 FFT, writes W (P/2 complex)
+        "fused3d_planes": P * s + P * s,    # 3D pass B: reads W, writes the field
         "gen_half": H * c,
         "line_c2c": 2 * H * c,
         "r2c_last_noise": H * c,
