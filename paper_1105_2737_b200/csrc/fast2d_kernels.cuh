@@ -193,6 +193,9 @@ struct HasPut2 : std::false_type {};
 #ifndef GRFC_GEN_NOBAR
 #define GRFC_GEN_NOBAR 1
 #endif
+#ifndef GRFC_ROW_NAMED
+#define GRFC_ROW_NAMED 1
+#endif
 #ifndef GRFC_ROW_WARPSYNC
 #define GRFC_ROW_WARPSYNC 1
 #endif
@@ -353,11 +356,14 @@ constexpr bool col_padded() {
 // with base mod PER = jj%NS); reads take jj + i N/R2 with jj < N/R2 likewise.
 // ALL: every team of the block owns a row (no predication).
 // WARP: the team of a row lies inside one warp (M/E <= 32 threads), so its
-// exchange needs only __syncwarp, never a CTA barrier.
-template <typename C, bool ALL = false, bool WARP = false>
+// exchange needs only __syncwarp, never a CTA barrier. NAMED > 0: the team is
+// NAMED whole warps and synchronises on its own hardware barrier (id `bar`),
+// so the teams of a tile do not wait for each other.
+template <typename C, bool ALL = false, bool WARP = false, int NAMED = 0>
 struct RowEx {
   C* s;
   bool active = true;  // idle teams (beyond the tile's rows) keep to the barriers only
+  int bar = 0;
   static constexpr int PER = 128 / (int)sizeof(C);
   __host__ __device__ __forceinline__ static constexpr int pad(int e) { return e + e / PER; }
   __device__ __forceinline__ bool on() const { return ALL || active; }
@@ -374,6 +380,8 @@ struct RowEx {
   __device__ __forceinline__ void sync() const {
     if constexpr (WARP)
       __syncwarp();
+    else if constexpr (NAMED > 0)
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NAMED) : "memory");
     else
       __syncthreads();
   }
@@ -700,7 +708,12 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
   // every team owns a row when the block holds exactly RPT teams (c2: 16 x 16 threads)
   constexpr bool ALL = NT == RPT * TT;
   constexpr bool WARP = GRFC_ROW_WARPSYNC && TT <= 32 && 32 % TT == 0;
-  RowEx<C, ALL, WARP> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(), ALL || rl < RPT};
+  // teams of whole warps (c3: 128 threads per 2048-point row) use one named
+  // barrier each (ids 1..teams; 0 is __syncthreads)
+  constexpr int TEAMS = (NT > 0 ? NT : RPT * TT) / TT;
+  constexpr int NAMED = (GRFC_ROW_NAMED && !WARP && TT % 32 == 0 && TEAMS <= 15) ? TT : 0;
+  RowEx<C, ALL, WARP, NAMED> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(),
+                                ALL || rl < RPT, 1 + rl};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   C* o = reinterpret_cast<C*>(of + (int64_t)row * (2 * M));
