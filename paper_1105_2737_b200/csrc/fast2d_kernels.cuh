@@ -522,6 +522,12 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 
 // Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
 // generation fused in front and the Z epilogue behind. Block = col_threads.
+// generation loop unroll of the fp32 column tiles (independent Philox chains in flight)
+#ifndef GRFC_GEN_UNROLL
+#define GRFC_GEN_UNROLL 4
+#endif
+constexpr int kGenUnroll = GRFC_GEN_UNROLL;
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -563,7 +569,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     const float K = p.f_sqrt_c * p.f_scale * 0.70710678118654752440f;
     const bool matern = p.family == GRFC_DENSITY_MATERN;
     const float A = 1.0f + p.f_ell2 * w2 * w2, B = K * ex2_approx(p.f_gauss_k * w2 * w2);
-#pragma unroll 2
+#pragma unroll (kGenUnroll)
     for (int t = 0; t < E / 2; ++t) {
       const int k1 = j + t * TT;
       const uint4 r = philox_draw(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col));
