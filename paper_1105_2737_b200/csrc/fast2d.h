@@ -21,6 +21,10 @@ struct Fast2D {
   double s_one = 1.0, s_two = 1.0;
   double l2_budget = 48.0 * 1024 * 1024;  // bytes of workspace per chunk
   void* d_tw = nullptr;                   // twiddles
+  // fp32 Algorithm 2: sqrt(g) x scale / sqrt 2 per half-lattice cell (n1 x (n2/2+1)),
+  // evaluated once per plan in fp64; nullptr when larger than kSgTableMax
+  float* d_sg = nullptr;
+  static constexpr size_t kSgTableMax = 8u << 20;
   int kind = 0;
   // persistent fused kernel geometry (fused_query)
   bool persistent = false;

@@ -401,6 +401,7 @@ struct F2Params {
   // fp32 copies for the SFU density path
   float f_wstep1, f_wstep2, f_sqrt_c, f_ell2, f_nhalf_alpha, f_gauss_k, f_scale;
   float f_lg2K;  // log2(sqrt_c * scale / sqrt 2) for the folded Matern multiplier
+  const float* sg;  // Fast2D::d_sg (fp32 Algorithm 2) or nullptr
   int family;
   DensityDesc D;
   GridDesc g;
@@ -559,7 +560,23 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // GRFC_EARLY_REL: release the previous tile before generation (its consumers
   // wait on it; the fence stalls warp 0 only while the others generate)
   if (GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
-  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
+  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && p.sg) {
+    // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one Philox
+    // call; sqrt(g) scale / sqrt 2 from the plan's per-cell table (L2-resident)
+    const float* __restrict__ sgc = p.sg + col;
+#pragma unroll(kGenUnroll)
+    for (int t = 0; t < E / 2; ++t) {
+      const int k1 = j + t * TT;
+      const float m0 = __ldg(&sgc[k1 * p.hd]), m1 = __ldg(&sgc[(k1 + N1 / 2) * p.hd]);
+      const uint4 r = philox_draw(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col));
+      float rad0, s0, c0, rad1, s1, c1;
+      box_muller_parts_f32(r.x, r.y, rad0, s0, c0);
+      box_muller_parts_f32(r.z, r.w, rad1, s1, c1);
+      const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
+      sm[k1 * SLOTS + slot] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
+    }
+  } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one
     // Philox call. sqrt(g) from the per-CTA row table rowq (fused2d_row_table):
     //   Matern   rowq = ell^2 w1^2:      m = K ex2(-alpha/2 lg2(A_col + rowq))
@@ -1086,6 +1103,7 @@ inline F2Params make_params(const Fast2D& f) {
   p.f_gauss_k = (float)(-0.25 * p.ell * p.ell * 1.4426950408889634);  // -ell^2/4 * log2(e)
   p.f_scale = (float)p.scale;
   p.f_lg2K = (float)std::log2(p.sqrt_c * p.scale * 0.70710678118654752440);
+  p.sg = f.d_sg;
   p.D = f.D;
   p.g = f.g;
   return p;

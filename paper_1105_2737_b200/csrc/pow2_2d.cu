@@ -162,6 +162,18 @@ static cudaError_t run_fast(const Fast2D& f, int alg, uint64_t seed, uint64_t fi
   return dispatch_rows<T>(f, nf, W, out, stride, s);
 }
 
+// sqrt(g(w_K)) * mult for every half-lattice cell, fp64 evaluation (the
+// generic device density, sqrt_gamma) rounded once to fp32.
+__global__ void k_sg_table(GridDesc g, DensityDesc D, double mult, float* __restrict__ out) {
+  const int64_t cells = g.n[0] * g.hd;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < cells; h += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k[2] = {h / g.hd, h % g.hd};
+    int64_t kw[2];
+    wrap_freq(g, k, kw);
+    out[h] = (float)(sqrt_gamma<double>(g, D, kw, h) * mult);
+  }
+}
+
 cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int dtype, int alg, double s_one,
                         double s_two) {
   f.n1 = (int)g.n[0];
@@ -186,6 +198,25 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
     e = cudaMemcpy(f.d_tw, a.data(), a.size() * cs, cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) return e;
+  // Density table of the fp32 Algorithm-2 column tiles: one L2-resident load per
+  // cell replaces the per-cell evaluation. Used for every family without an SFU
+  // form (otherwise evaluated per cell in fp64), and for Matern / Gaussian when
+  // the columns are long enough to hide the load (N1 >= 1024: c5 245 -> 254
+  // Gpts/s; at N1 = 512 the SFU form is faster, 292 vs 286). GRFC_SG_TABLE=0/1
+  // forces it off/on.
+  const size_t sg_bytes = (size_t)f.n1 * (size_t)(f.n2 / 2 + 1) * sizeof(float);
+  const char* sge = std::getenv("GRFC_SG_TABLE");
+  const bool sfu_family = D.family == GRFC_DENSITY_MATERN || D.family == GRFC_DENSITY_GAUSSIAN_COV;
+  const bool want_sg = sge ? sge[0] == '1' : (!sfu_family || f.n1 >= 1024);
+  if (dtype == GRFC_F32 && alg == GRFC_ONE_FFT_OVERWRITE && sg_bytes <= Fast2D::kSgTableMax && want_sg) {
+    f.fail_what = "density table";
+    e = cudaMalloc(&f.d_sg, sg_bytes);
+    if (e != cudaSuccess) return e;
+    k_sg_table<<<148, 256>>>(g, D, s_one * 0.70710678118654752440, f.d_sg);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+  }
   // Pipeline chunk: ~12 MiB of half-spectrum per slot, 3 slots in flight (L2-resident).
   const double slot = (double)f.n1 * (f.n2 / 2) * cs;
   f.chunk = (int64_t)std::max(1.0, std::floor(12.0 * 1024 * 1024 / slot));
@@ -232,6 +263,8 @@ size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf) {
 void fast2d_free(Fast2D& f) {
   cudaFree(f.d_tw);
   f.d_tw = nullptr;
+  cudaFree(f.d_sg);
+  f.d_sg = nullptr;
   if (f.sa) cudaStreamDestroy(f.sa);
   if (f.sb) cudaStreamDestroy(f.sb);
   cudaEvent_t evs[] = {f.ev_fork, f.ev_ja, f.ev_jb};
