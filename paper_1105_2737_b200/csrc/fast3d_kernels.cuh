@@ -102,8 +102,33 @@ __device__ __forceinline__ C_t<T> gen_cell3(const F3Params& p, int k0, int k1, i
 // slot = h*2CB + side*CB + c. Zh partner of (h, side, c) is (1-h, 1-side, c);
 // strip 0 exceptions: column 0's partner is the Nyquist column M of -k1 (kept
 // in an extra shared column per h), column M/2's partner is (1-h, R, 0).
+// Resident pass-A / pass-B CTAs per SM the fp32 kernels are compiled for
+// (register budget; fp64 lets ptxas choose). 512^3 fp32: pass A 2 CTAs of 512
+// threads at 64 registers (0.599 -> 0.515 ms), pass B 4 CTAs at 64 registers
+// (0.521 -> 0.432 ms), both without spills.
+#ifndef GRFC_COLGEN3_MINB
+#define GRFC_COLGEN3_MINB 2
+#endif
+#ifndef GRFC_PLANES_MINB
+#define GRFC_PLANES_MINB 4
+#endif
+// (capped so every thread keeps >= 64 registers; plans with 32-element rows keep
+// ptxas's choice)
+constexpr int minb_cap(int want, int threads) {
+  return want < 65536 / (threads * 64) ? want : 65536 / (threads * 64);
+}
+template <typename T, int N0>
+constexpr int colgen3_min_blocks() {
+  return sizeof(T) == 4 ? minb_cap(GRFC_COLGEN3_MINB, colgen3_threads<N0, T>()) : 1;
+}
+template <typename T, int N1, int M>
+constexpr int planes_min_blocks() {
+  return (sizeof(T) == 4 && RowPlan<M, T>::E <= 16 && ColPlan<N1, T>::E <= 16)
+             ? minb_cap(GRFC_PLANES_MINB, col_threads<N1, T>())
+             : 0;
+}
 template <typename T, int N0, int ALG>
-__global__ void __launch_bounds__(colgen3_threads<N0, T>(), 1)
+__global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T, N0>())
     k_3d_colgen(F3Params p, PhiloxKey key, uint64_t fld, C_t<T>* __restrict__ W, int k1_lo, int k1_cnt,
                 const C_t<T>* __restrict__ tw0, const C_t<T>* __restrict__ tw2) {
   using C = C_t<T>;
@@ -218,7 +243,7 @@ constexpr int rows3_per_tile() {
 // Pass B: persistent over this rank's planes (same ticket/ring scheme as
 // k_fused2d: C(p) tiles = axis-1 strips, R(p) tiles = rows).
 template <typename T, int N1, int M>
-__global__ void __launch_bounds__(col_threads<N1, T>())
+__global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1, M>())
     k_3d_planes(F2Sched q, const C_t<T>* __restrict__ src, int n0_per, int n1_per, C_t<T>* __restrict__ ring,
                 T* __restrict__ out, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
