@@ -88,7 +88,10 @@ GRFC_PLAN(ColPlan, 512, float, 16, 8, 16, 16, 2)
 #else
 GRFC_PLAN(ColPlan, 512, float, 32, 8, 32, 16)
 #endif
-GRFC_PLAN(ColPlan, 1024, float, 32, 8, 32, 32)
+#ifndef GRFC_COL1024_X
+#define GRFC_COL1024_X 4
+#endif
+GRFC_PLAN(ColPlan, 1024, float, 32, GRFC_COL1024_X, 32, 32)
 GRFC_PLAN(ColPlan, 2048, float, 16, 4, 16, 16, 8)
 #ifndef GRFC_COL4096_X
 #define GRFC_COL4096_X 2
@@ -836,6 +839,9 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 #ifndef GRFC_TILE_STATS_BUILD
 #define GRFC_TILE_STATS_BUILD 0
 #endif
+#ifndef GRFC_FUSED1024_MINB
+#define GRFC_FUSED1024_MINB 2
+#endif
 #ifndef GRFC_FUSED_MINB
 #define GRFC_FUSED_MINB 4
 #endif
@@ -843,6 +849,7 @@ template <int N1, int M, typename T>
 constexpr int fused_min_blocks() {
   return (N1 == 512 && sizeof(T) == 4) ? GRFC_FUSED_MINB
          : (N1 == 4096 && sizeof(T) == 4 && ColPlan<N1, T>::X == 1) ? 2
+         : (N1 == 1024 && sizeof(T) == 4 && ColPlan<N1, T>::X == 4) ? GRFC_FUSED1024_MINB
                                                                     : 0;
 }
 template <typename T, int N1, int M, int ALG>
