@@ -199,7 +199,7 @@ def run_reference_arm(args, cfg):
                                    f"xoshiro substreams (0, j)), one field per std::thread"},
         "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ our arm
@@ -408,7 +408,7 @@ def run_ours(args, cfg):
             "roofline": roofline, "compute_roofline": compute, "kernels": kernels, "alg1": alg1, "e2e": e2e, "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -495,11 +495,31 @@ def run_slab(args, cfg):
                     "d2h_bytes_per_step": P * 4, "ms_per_step": float(te.item())},
             "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "cpu_baseline": None,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout (see main)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    global _JSON_FD
+    # Library banners written to fd 1 from C code (e.g. NCCL's version line at
+    # communicator creation) would precede the JSON line: route fd 1 to stderr for
+    # the run and keep the original stdout for the result alone.
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

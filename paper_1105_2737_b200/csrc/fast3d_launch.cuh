@@ -87,7 +87,7 @@ cudaError_t launch_3d_planes(const Fast3D& f, const void* src, int n0p, int n1p,
   constexpr size_t smem = planes_smem<N1, M, T>();
   F2Sched q{};
   uint32_t conc = 0;
-  ring_geometry(f.sms, f.occ, f.strips, f.rtiles, n0p, &q.L, &q.S, &conc);
+  ring_geometry(f.sms, f.occ, f.strips, f.rtiles, n0p, &q.L, &q.S, &conc, 3, 2);
   q.F = (uint32_t)n0p;
   q.strips = (uint32_t)f.strips;
   q.rtiles = (uint32_t)f.rtiles;

@@ -136,7 +136,7 @@ cudaError_t fast3d_pass_a(const Fast3D& f, int world, int rank, uint64_t seed, u
 
 static size_t planes_ws_bytes(const Fast3D& f, int n0p) {
   uint32_t L, S, c;
-  ring_geometry(f.sms, f.occ, f.strips, f.rtiles, n0p, &L, &S, &c);
+  ring_geometry(f.sms, f.occ, f.strips, f.rtiles, n0p, &L, &S, &c, 3, 2);
   return fused_ctr_bytes(S) + (size_t)S * f.n1 * (f.n2 / 2) * (f.dtype == GRFC_F64 ? 16 : 8);
 }
 
