@@ -50,14 +50,9 @@ inline void ring_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, 
   // Defaults: 12 / 8 for the 2D generator (its column tiles are ~2x its row tiles
   // and a deep ring absorbs the imbalance), 3 / 2 for the 3D pass B (balanced
   // plain-FFT tiles: an L2-sized plane ring wins, 0.429 -> 0.390 ms at 512^3).
-  static const int la_env = [] {
-    const char* e = std::getenv("GRFC_RING_LA");
-    return e ? std::atoi(e) : -1;
-  }();
-  static const int sl_env = [] {
-    const char* e = std::getenv("GRFC_RING_SL");
-    return e ? std::atoi(e) : -1;
-  }();
+  const char* ela = std::getenv("GRFC_RING_LA");
+  const char* esl = std::getenv("GRFC_RING_SL");
+  const int la_env = ela ? std::atoi(ela) : -1, sl_env = esl ? std::atoi(esl) : -1;
   const uint32_t la = la_env >= 0 ? (uint32_t)la_env : la_def;
   const uint32_t sl = sl_env >= 0 ? (uint32_t)sl_env : sl_def;
   const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + rtiles);
