@@ -85,7 +85,7 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
 template <typename T, int N1>
 __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                               const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
-                                              unsigned char* smem_raw, const float* __restrict__ rowq,
+                                              unsigned char* smem_raw,
                                               uint32_t* sig = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
@@ -143,42 +143,35 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
       for (int i = 0; i < RL; ++i) sm[(j + b * TT + i * (N1 / RL)) * SLOTS + slot] = v[b * RL + i];
     __syncthreads();
     // 4. V = U sqrt(g) scale, then Zh with the mirrored partner V(-k1, M-col).
-    // fp32 Matern / Gaussian interior columns: sqrt(g) from the per-CTA row table
-    // (fused2d_row_table; rowq is even in k1, so row -k1 reuses rowq[k1]) and the
-    // two columns' factors, as Algorithm 2's col_tile does.
     const T sc = (T)p.scale;
-    const bool fast_dens = sizeof(T) == 4 && rowq && !packed;
-    float Ac = 0.f, Ap = 0.f, Bc = 0.f, Bp = 0.f;
-    const bool matern = p.family == GRFC_DENSITY_MATERN;
-    if (fast_dens) {
-      const int pc = mid ? col : pcol;
-      const float wc = (float)(col <= p.n2 / 2 ? col : col - p.n2) * p.f_wstep2;
-      const float wp = (float)(pc <= p.n2 / 2 ? pc : pc - p.n2) * p.f_wstep2;
-      Ac = 1.0f + p.f_ell2 * wc * wc;
-      Ap = 1.0f + p.f_ell2 * wp * wp;
-      Bc = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wc * wc);
-      Bp = p.f_sqrt_c * p.f_scale * ex2_approx(p.f_gauss_k * wp * wp);
-    }
-    const float Km = p.f_sqrt_c * p.f_scale;
+    // fp32: sqrt(g) x scale from the plan's table (always present for fp32 Algorithm 1)
+    const float* __restrict__ sgk = p.sg + (packed ? 0 : col);
+    const float* __restrict__ sgm = p.sg + (packed ? p.m : (mid ? col : pcol));
+    const int uslot = (packed || mid) ? slot : pslot;
   #pragma unroll
     for (int b = 0; b < E / R0; ++b)
   #pragma unroll
       for (int i = 0; i < R0; ++i) {
         const int k1 = j + b * TT + i * (N1 / R0), km = (N1 - k1) & (N1 - 1);
         C Vk, Vm;
-        if (packed) {
+        if constexpr (sizeof(T) == 4) {
+          const float mk_ = __ldg(&sgk[k1 * p.hd]), mm_ = __ldg(&sgm[km * p.hd]);
+          const C Uk = sm[k1 * SLOTS + slot], Um = sm[km * SLOTS + uslot];
+          if (packed) {
+            // F0(k1) = (U(k1) + conj U(-k1))/2 ; FM(-k1) = -i (U(-k1) - conj U(k1))/2
+            Vk = cscale(mk<C>((Uk.x + Um.x) * half, (Uk.y - Um.y) * half), (T)mk_);
+            Vm = cscale(mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half), (T)mm_);
+          } else {
+            Vk = cscale(Uk, (T)mk_);
+            Vm = cscale(Um, (T)mm_);
+          }
+        } else if (packed) {
           const C Uk = sm[k1 * SLOTS + slot], Um = sm[km * SLOTS + slot];
           // F0(k1) = (U(k1) + conj U(-k1))/2 ; FM(-k1) = -i (U(-k1) - conj U(k1))/2
           const C F0k = mk<C>((Uk.x + Um.x) * half, (Uk.y - Um.y) * half);
           const C FMm = mk<C>((Um.y + Uk.y) * half, -(Um.x - Uk.x) * half);
           Vk = cscale(F0k, sqrt_g2<T>(p, k1, 0) * sc);
           Vm = cscale(FMm, sqrt_g2<T>(p, km, p.m) * sc);
-        } else if (fast_dens) {
-          const float q = rowq[k1];
-          const float mk_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ac + q)) : Bc * q;
-          const float mm_ = matern ? Km * ex2_approx(p.f_nhalf_alpha * lg2_approx(Ap + q)) : Bp * q;
-          Vk = cscale(sm[k1 * SLOTS + slot], (T)mk_);
-          Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], (T)mm_);
         } else {
           Vk = cscale(sm[k1 * SLOTS + slot], sqrt_g2<T>(p, k1, col) * sc);
           Vm = cscale(sm[km * SLOTS + (mid ? slot : pslot)], sqrt_g2<T>(p, km, mid ? col : pcol) * sc);
@@ -197,11 +190,12 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
 }
 
 #ifndef GRFC_ALG1_MINB
-#define GRFC_ALG1_MINB 4
+#define GRFC_ALG1_MINB 3
 #endif
-// Four resident 256-thread CTAs per SM for the fp32 shapes (64 registers; the few
-// spills cost less than the lost occupancy: 512 x 256 Alg 1 121 -> 125 Gpts/s vs
-// three CTAs at 80 registers, 101 with two); larger blocks / fp64 let ptxas choose.
+// Three resident 256-thread CTAs per SM for the fp32 shapes (80 registers, no
+// spills now that the column tile reads sqrt(g) from the plan's table: 512 x 512
+// Alg 1 136 Gpts/s vs 128 with four CTAs at 64 registers and spills); larger
+// blocks / fp64 let ptxas choose.
 template <int N1, int M, typename T>
 constexpr int alg1_min_blocks() {
   return (sizeof(T) == 4 && fused_threads<N1, M, T>() <= 256) ? GRFC_ALG1_MINB : 0;
@@ -212,10 +206,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
                    T* __restrict__ out, int64_t out_stride, const C_t<T>* __restrict__ tw1,
                    const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ float s_rowq[N1];
   constexpr int RPT = rows_per_tile<N1, M, T>();
-  const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
-  if (table) fused2d_row_table<N1>(p, s_rowq);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t L = q.L, F = q.F, g1 = q.g1, gc = q.gc, g2 = q.g2;
   // ticket ranges (L <= F/2): [0,L): R1 | [L,2L): R1 C | [2L,F): R1 C R2 | [F,F+L): C R2 | [F+L,F+2L): R2
@@ -315,7 +306,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
       r1_tile<T, N1, M, RPT>(p, key, field0 + m.f, (int)m.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr);
       done_ctr = &q.r1_done[m.slot];
     } else if (m.kind == 1) {
-      alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, done_ctr);
+      alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, done_ctr);
       done_ctr = &q.col_done[m.slot];
     } else {
       row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
