@@ -208,7 +208,7 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   const char* sge = std::getenv("GRFC_SG_TABLE");
   const bool sfu_family = D.family == GRFC_DENSITY_MATERN || D.family == GRFC_DENSITY_GAUSSIAN_COV;
   const bool want_sg = sge ? sge[0] == '1' : (!sfu_family || f.n1 >= 1024);
-  // The fp32 Algorithm-1 kernel always uses the table (sqrt(g) x scale, no 1/sqrt 2):
+  // The fp32 Algorithm-1 kernel always uses the table (sqrt(g) x its scale s_two):
   // its column tile then holds no per-cell density code at all (the inlined fp64
   // fallbacks made the kernel 48k instructions long: I-cache misses).
   const bool alg1_f32 = dtype == GRFC_F32 && alg == GRFC_TWO_FFT;
@@ -217,7 +217,7 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
     f.fail_what = "density table";
     e = cudaMalloc(&f.d_sg, sg_bytes);
     if (e != cudaSuccess) return e;
-    k_sg_table<<<148, 256>>>(g, D, alg1_f32 ? s_one : s_one * 0.70710678118654752440, f.d_sg);
+    k_sg_table<<<148, 256>>>(g, D, alg1_f32 ? s_two : s_one * 0.70710678118654752440, f.d_sg);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return e;
