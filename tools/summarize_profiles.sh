@@ -2,6 +2,7 @@
 # Turn the ncu reports of tools/profile_all.sh into text summaries under
 # gpurun_out/summaries/ (run on the box: the reports are too large to copy back).
 cd "$(dirname "$0")/.."
+export PATH=/usr/local/cuda/bin:$PATH
 R=${ROUND:-r01}; O=paper_1105_2737_b200/build; D=gpurun_out/summaries
 mkdir -p $D
 mk() { # rep obj kernel out
