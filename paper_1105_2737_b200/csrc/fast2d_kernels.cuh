@@ -532,6 +532,27 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 #endif
 constexpr int kGenUnroll = GRFC_GEN_UNROLL;
 
+// Group-per-column column tiles (see col_tile): fp32 plans whose column team is
+// several whole warps (N1/E > 32, c3: 256 threads per 4096-point column): each
+// column's FFT synchronises on its own named barrier, so the 4 columns of a tile
+// (one CTA per SM) do not wait for each other; one CTA barrier hands the results to
+// the epilogue. (One warp per column, N1/E = 32, measured slower on c2: 282 vs 291.)
+#ifndef GRFC_COLGROUP
+#define GRFC_COLGROUP 1
+#endif
+template <int N1, typename T>
+constexpr bool col_warp_mode() {
+  return GRFC_COLGROUP && sizeof(T) == 4 && N1 / ColPlan<N1, T>::E > 32 && (N1 / ColPlan<N1, T>::E) % 32 == 0 &&
+         2 * ColPlan<N1, T>::X <= 15 && 2 * ColPlan<N1, T>::X * (N1 / ColPlan<N1, T>::E) == col_threads<N1, T>();
+}
+// per-column region: N1 padded rows + 4 elements (so the regions start 8 banks apart)
+constexpr int wcol_pitch(int n1) { return n1 + n1 / 16 + 4; }
+
+template <typename T, int N1, int MC>
+__device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
+                                             const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
+                                             int col, bool packed, bool mid);
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -549,13 +570,22 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
   constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
-  const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
+  // WCOL: warp w owns column slot w (one column per warp, team = the warp's 32
+  // lanes): the column FFT's exchanges are warp-private (__syncwarp) in a padded
+  // per-warp region, and one CTA barrier hands the results to the epilogue's
+  // slot-across-lanes mapping (coalesced W stores, shuffle partner pairing).
+  constexpr bool WCOL = col_warp_mode<N1, T>();
+  constexpr int GTT = N1 / E;  // threads per column group (one warp or several: named barrier)
+  const int tid = threadIdx.x;
+  const int slot = WCOL ? tid / GTT : tid % SLOTS, j = WCOL ? tid % GTT : tid / SLOTS;
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);
 
   // Generation into shared memory (rolled loop: one copy of the Philox/Box-
   // Muller/density code in the I-cache). Thread j owns rows j + t*TT.
   C* sm = reinterpret_cast<C*>(smem_raw);
+  C* const rg = sm + slot * wcol_pitch(N1);  // WCOL: this warp's region
+  auto gslot = [&](int k1) -> C& { return WCOL ? rg[RowEx<C>::pad(k1)] : sm[k1 * SLOTS + slot]; };
   // Thread 0 reads the slot's "previous rows consumed" counter now (relaxed);
   // it is only needed before the W stores, so its latency hides behind the tile.
   uint32_t dep_seen = 0;
@@ -576,8 +606,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       box_muller_parts_f32(r.x, r.y, rad0, s0, c0);
       box_muller_parts_f32(r.z, r.w, rad1, s1, c1);
       const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
-      sm[k1 * SLOTS + slot] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
-      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
+      gslot(k1) = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      gslot(k1 + N1 / 2) = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
     }
   } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one
@@ -601,8 +631,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       const float m0 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q0), p.f_lg2K)) : B * q0;
       const float m1 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q1), p.f_lg2K)) : B * q1;
       const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
-      sm[k1 * SLOTS + slot] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
-      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
+      gslot(k1) = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      gslot(k1 + N1 / 2) = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
     }
   } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
     const T r = (T)0.70710678118654752440, sc = (T)p.scale;
@@ -612,8 +642,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       float a0, b0, a1, b1;
       unit_quad_f32(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col), a0, b0, a1, b1);
       const T m0 = sqrt_g2<T>(p, k1, col) * sc * r, m1 = sqrt_g2<T>(p, k1 + N1 / 2, col) * sc * r;
-      sm[k1 * SLOTS + slot] = mk<C>((T)a0 * m0, -(T)b0 * m0);
-      sm[(k1 + N1 / 2) * SLOTS + slot] = mk<C>((T)a1 * m1, -(T)b1 * m1);
+      gslot(k1) = mk<C>((T)a0 * m0, -(T)b0 * m0);
+      gslot(k1 + N1 / 2) = mk<C>((T)a1 * m1, -(T)b1 * m1);
     }
   } else {
 #pragma unroll 1
@@ -624,7 +654,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
         const C y = gen_cell<T, ALG>(p, k1, p.m, key, fld);
         x = mk<C>(x.x - y.y, x.y + y.x);
       }
-      sm[k1 * SLOTS + slot] = x;
+      gslot(k1) = x;
     }
   }
   // Every thread reads back exactly the rows it generated (rows j + u TT, the
@@ -639,19 +669,57 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
 #pragma unroll
-    for (int i = 0; i < R0; ++i) v[b * R0 + i] = sm[(j + b * TT + i * (N1 / R0)) * SLOTS + slot];
-  __syncthreads();
-  using Ex = std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
-  Ex ex{sm, slot};
-  // The slot's previous field must be consumed before W is overwritten: checked
-  // at the FFT's exchange barriers (all W stores follow the last one).
-  constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
-  if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
-  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
-  if (dep && !has_ex) {
-    if (threadIdx.x == 0 && dep_seen < dep_target)
-      while (ld_relaxed_u32(dep) < dep_target) __nanosleep(256);
+    for (int i = 0; i < R0; ++i) v[b * R0 + i] = gslot(j + b * TT + i * (N1 / R0));
+  if constexpr (WCOL) {
+    RowEx<C, true, GTT == 32, (GTT > 32 ? GTT : 0)> wex{rg, true, 1 + slot};
+    wex.sync();  // own rows read back: the group's first exchange may overwrite them
+    line_fft<N1, E, +1>(v, j, tw1, 1, wex, typename PL::R{});
+    // results to the region in natural row order, then one CTA barrier (thread 0
+    // first checks the ring-slot reuse dependency: every W store follows it)
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) rg[RowEx<C>::pad(j + b * TT + i * (N1 / RL))] = v[b * RL + i];
+    LateDep{dep, dep_target, dep_seen, 0}.check();
     __syncthreads();
+  } else {
+    __syncthreads();
+    using Ex = std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
+    Ex ex{sm, slot};
+    // The slot's previous field must be consumed before W is overwritten: checked
+    // at the FFT's exchange barriers (all W stores follow the last one).
+    constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
+    if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
+    line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    if (dep && !has_ex) {
+      if (threadIdx.x == 0 && dep_seen < dep_target)
+        while (ld_relaxed_u32(dep) < dep_target) __nanosleep(256);
+      __syncthreads();
+    }
+  }
+  col_epilogue<T, N1, MC>(p, s, Wf, tw2, sm, v, slot, j, col, packed, mid);
+}
+
+// Z epilogue + W stores of a column tile, lanes across the strip's slots
+// (slot = tid % SLOTS, team position j = tid / SLOTS). In WCOL mode the FFT
+// results are re-read here from the per-warp regions in that mapping.
+template <typename T, int N1, int MC>
+__device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
+                                             const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
+                                             int col, bool packed, bool mid) {
+  using C = C_t<T>;
+  using PL = ColPlan<N1, T>;
+  constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
+  constexpr int RL = RLast<typename PL::R>::value;
+  if constexpr (col_warp_mode<N1, T>()) {
+    slot = threadIdx.x % SLOTS;
+    j = threadIdx.x / SLOTS;
+    col = slot_column(s, slot, CB, p.m, packed, mid);
+    const C* rgs = sm + slot * wcol_pitch(N1);
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) v[b * RL + i] = rgs[RowEx<C>::pad(j + b * TT + i * (N1 / RL))];
   }
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
   const bool special = packed || mid;
@@ -766,7 +834,9 @@ constexpr int rows_per_tile() {
 template <int N1, int M, typename T>
 constexpr size_t fused_smem() {
   using C = C_t<T>;
-  constexpr size_t a = (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t a = col_warp_mode<N1, T>()
+                           ? (size_t)wcol_pitch(N1) * 2 * ColPlan<N1, T>::X * sizeof(C)
+                           : (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
   constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
   return a > b ? a : b;
 }
@@ -1121,7 +1191,8 @@ cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t
                                cudaStream_t s) {
   using C = C_t<T>;
   constexpr int CB = ColPlan<N1, T>::X;
-  const size_t smem = (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
+  const size_t smem = col_warp_mode<N1, T>() ? (size_t)wcol_pitch(N1) * 2 * CB * sizeof(C)
+                                             : (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_cols_gen<T, N1, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
