@@ -24,10 +24,18 @@ def main(rep, obj, kname, top=40):
     iextra = [hdr.index(h) for h in extra]
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True)
-    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    lines = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True,
-                           text=True).stdout.split("\n")
-    start = next(i for i, l in enumerate(lines) if l.strip().startswith(".section") and kname in l)
+    # obj may be one object or the linked library (several cubins): use the cubin
+    # that holds the kernel
+    lines, start = None, None
+    for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+        ls = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True,
+                            text=True).stdout.split("\n")
+        st = next((i for i, l in enumerate(ls) if l.strip().startswith(".section") and kname in l), None)
+        if st is not None:
+            lines, start = ls, st
+            break
+    if lines is None:
+        raise SystemExit(f"kernel {kname} not found in {obj}")
     cur, m = None, {}
     for l in lines[start + 1:]:
         if l.strip().startswith(".section"):
