@@ -99,7 +99,12 @@ GRFC_PLAN(ColPlan, 2048, float, 16, 4, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, float, 16, GRFC_COL4096_X, 16, 16, 16)
 GRFC_PLAN(ColPlan, 128, double, 16, 4, 16, 8)
 GRFC_PLAN(ColPlan, 256, double, 16, 8, 16, 16)
-GRFC_PLAN(ColPlan, 512, double, 16, 8, 16, 16, 2)
+// fp64 512-point columns: 2 column pairs per 128-thread tile (c1, one 512^2 field:
+// 64 column tiles instead of 16 spread the fp64 generation over more SMs, 55 -> 36 us)
+#ifndef GRFC_COL512D_X
+#define GRFC_COL512D_X 2
+#endif
+GRFC_PLAN(ColPlan, 512, double, 16, GRFC_COL512D_X, 16, 16, 2)
 GRFC_PLAN(ColPlan, 1024, double, 16, 4, 16, 16, 4)
 GRFC_PLAN(ColPlan, 2048, double, 16, 2, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, double, 16, 1, 16, 16, 16)
