@@ -41,7 +41,10 @@ struct ColPlan3 {
   };
 GRFC_PLAN3(128, float, 16, 4, 16, 8)
 GRFC_PLAN3(256, float, 16, 4, 16, 16)
-GRFC_PLAN3(512, float, 16, 4, 16, 16, 2)
+#ifndef GRFC_COL3_512_X
+#define GRFC_COL3_512_X 4
+#endif
+GRFC_PLAN3(512, float, 16, GRFC_COL3_512_X, 16, 16, 2)
 GRFC_PLAN3(1024, float, 16, 4, 16, 16, 4)
 GRFC_PLAN3(128, double, 16, 2, 16, 8)
 GRFC_PLAN3(256, double, 16, 2, 16, 16)
