@@ -152,8 +152,48 @@ __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T
 
   // generation (rolled loop): X(k0, k1, col) for k0 = j + t TT
   const bool fast = ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && col != 0 && col != p.m;
-  if (fast) {
-    // interior column: own draws; rows k0 and k0 + N0/2 are units u and u + Uh
+  // per-CTA axis-0 density table (fp32 Matern / Gaussian)
+  __shared__ float s_q0[sizeof(T) == 4 ? N0 : 1];
+  const float* q0 = nullptr;
+  if constexpr (sizeof(T) == 4) {
+    if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
+      for (int k = threadIdx.x; k < N0; k += blockDim.x) {
+        const int w0i = k <= p.n0 / 2 ? k : k - p.n0;
+        const float a0 = (float)w0i * p.f_wstep[0];
+        s_q0[k] = p.family == GRFC_DENSITY_MATERN ? p.f_ell2 * a0 * a0 : ex2_approx(p.f_gauss_k * a0 * a0);
+      }
+      __syncthreads();
+      q0 = s_q0;
+    }
+  }
+  if (fast && q0) {
+    // interior column, Matern / Gaussian: rows k0 and k0 + N0/2 are units u and
+    // u + Uh (one Philox call); the (k1, col) part of |w|^2 is per-thread and the
+    // k0 part comes from the per-CTA table q0 (as the 2D column tile's rowq):
+    //   Matern   q0 = ell^2 w0^2:                 m = ex2(-alpha/2 lg2(A + q0) + lg2(sqrt_c K))
+    //   Gaussian q0 = ex2(-ell^2 w0^2/4 log2 e):  m = B q0
+    const float K = p.f_scale * 0.70710678118654752440f;  // sqrt_g3 includes sqrt(c)
+    const int w1i = k1 <= p.n1 / 2 ? k1 : k1 - p.n1, w2i = col <= p.n2 / 2 ? col : col - p.n2;
+    const float b = (float)w1i * p.f_wstep[1], cc = (float)w2i * p.f_wstep[2], bc2 = b * b + cc * cc;
+    const bool matern = p.family == GRFC_DENSITY_MATERN;
+    const float A = 1.0f + p.f_ell2 * bc2, B = p.f_sqrt_c * K * ex2_approx(p.f_gauss_k * bc2);
+    const float lgK = lg2_approx(p.f_sqrt_c * K);
+#pragma unroll 4
+    for (int t = 0; t < E / 2; ++t) {
+      const int k0 = j + t * TT;
+      const uint4 r = philox_draw(key, fld, (uint64_t)(((uint32_t)k0 * p.n1 + k1) * p.hd + col));
+      float rad0, s0, c0, rad1, s1, c1;
+      box_muller_parts_f32(r.x, r.y, rad0, s0, c0);
+      box_muller_parts_f32(r.z, r.w, rad1, s1, c1);
+      const float qa = q0[k0], qb = q0[k0 + N0 / 2];
+      const float m0 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + qa), lgK)) : B * qa;
+      const float m1 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + qb), lgK)) : B * qb;
+      const float g0 = rad0 * m0, g1 = rad1 * m1;
+      sm[k0 * PITCH + slot] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      sm[(k0 + N0 / 2) * PITCH + slot] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
+    }
+  } else if (fast) {
+    // interior column, other families
     const float K = p.f_scale * 0.70710678118654752440f;  // sqrt_g3 includes sqrt(c)
 #pragma unroll 2
     for (int t = 0; t < E / 2; ++t) {
