@@ -270,7 +270,7 @@ __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int
       const int r = k1 / n1_per, k1l = k1 - r * n1_per;
       v[b * R0 + i] = __ldcs(&src[(((int64_t)r * n0_per + j0l) * n1_per + k1l) * m + col]);
     }
-  ColEx<C, SLOTS> ex{reinterpret_cast<C*>(smem_raw), slot};
+  std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{reinterpret_cast<C*>(smem_raw), slot};
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1,
 template <int N1, int M, typename T>
 constexpr size_t planes_smem() {
   using C = C_t<T>;
-  constexpr size_t a = (size_t)N1 * 2 * ColPlan<N1, T>::X * sizeof(C);
+  constexpr size_t a = (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * ColPlan<N1, T>::X * sizeof(C);
   constexpr size_t b = (size_t)rows_per_tile<N1, M, T>() * row_pitch<M, C>() * sizeof(C);
   return a > b ? a : b;
 }
