@@ -200,14 +200,13 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   if (e != cudaSuccess) return e;
   // Density table of the fp32 Algorithm-2 column tiles: one L2-resident load per
   // cell replaces the per-cell evaluation. Used for every family without an SFU
-  // form (otherwise evaluated per cell in fp64), and for Matern / Gaussian when
-  // the columns are long enough to hide the load (N1 >= 1024: c5 245 -> 254
-  // Gpts/s; at N1 = 512 the SFU form is faster, 292 vs 286). GRFC_SG_TABLE=0/1
-  // forces it off/on.
+  // form (otherwise evaluated per cell in fp64); Matern / Gaussian keep the SFU
+  // form, which measured faster (c2 292 vs 286, c5 273 vs 269 Gpts/s).
+  // GRFC_SG_TABLE=0/1 forces it off/on.
   const size_t sg_bytes = (size_t)f.n1 * (size_t)(f.n2 / 2 + 1) * sizeof(float);
   const char* sge = std::getenv("GRFC_SG_TABLE");
   const bool sfu_family = D.family == GRFC_DENSITY_MATERN || D.family == GRFC_DENSITY_GAUSSIAN_COV;
-  const bool want_sg = sge ? sge[0] == '1' : (!sfu_family || f.n1 >= 1024);
+  const bool want_sg = sge ? sge[0] == '1' : !sfu_family;
   // The fp32 Algorithm-1 kernel always uses the table (sqrt(g) x its scale s_two):
   // its column tile then holds no per-cell density code at all (the inlined fp64
   // fallbacks made the kernel 48k instructions long: I-cache misses).
