@@ -326,11 +326,16 @@ inline size_t alg1_ctr_bytes(uint32_t S) { return ((1 + 3 * (size_t)S) * 4 + 255
 
 inline void alg1_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, uint32_t* L, uint32_t* S,
                           uint32_t* conc) {
+  // lookahead LA x (tiles all resident CTAs run at once) / (tiles per field) between
+  // consecutive stages; slots = 2 lookaheads + SL x that + 2 (GRFC_ALG1_LA / _SL override)
+  const char* ela = std::getenv("GRFC_ALG1_LA");
+  const char* esl = std::getenv("GRFC_ALG1_SL");
+  const uint32_t la = ela ? (uint32_t)std::atoi(ela) : 5u, sl = esl ? (uint32_t)std::atoi(esl) : 4u;
   const uint32_t c = (uint32_t)(sms * occ), G = (uint32_t)(strips + 2 * rtiles);
-  uint32_t l = (5 * c + G - 1) / G;  // + the two tickets each CTA reserves ahead
+  uint32_t l = (la * c + G - 1) / G;  // + the two tickets each CTA reserves ahead
   l = l < 1 ? 1 : l;
   l = l < (uint32_t)(nf / 2) ? l : (uint32_t)(nf / 2);
-  uint32_t s = 2 * l + 4 * ((c + G - 1) / G) + 2;
+  uint32_t s = 2 * l + sl * ((c + G - 1) / G) + 2;
   s = s < (uint32_t)nf ? s : (uint32_t)nf;
   *L = l;
   *S = s;
