@@ -189,6 +189,9 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
     for (int i = 0; i < RL; ++i) __stcg(&Wf[(int64_t)(j + b * TT + i * (N1 / RL)) * p.m + col], v[b * RL + i]);
 }
 
+#ifndef GRFC_ALG1_RES1
+#define GRFC_ALG1_RES1 1
+#endif
 #ifndef GRFC_ALG1_MINB
 #define GRFC_ALG1_MINB 3
 #endif
@@ -267,27 +270,40 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
       const uint32_t* ctr;
       const uint32_t target = dep_of(x, ctr);
       if (target) {
-        if (v < target) v = ld_relaxed_u32(ctr);
-        m.ready = v >= target;
-        if (m.ready && x.kind != 0) (void)ld_acquire_u32(ctr);
+        if (GRFC_ALG1_RES1 && x.kind != 0) {
+          m.ready = ld_acquire_u32(ctr) >= target;  // one round trip: checks and orders
+        } else {
+          if (v < target) v = ld_relaxed_u32(ctr);
+          m.ready = v >= target;
+          if (m.ready && x.kind != 0) (void)ld_acquire_u32(ctr);
+        }
       }
     }
     s_msg = m;
   };
+  // GRFC_ALG1_RES1: one reservation (the next ticket is claimed at the top of a
+  // tile and read at its end), as k_fused2d; otherwise two reserved tickets with
+  // early relaxed dependency loads.
   if (threadIdx.x == 0) {
     const uint32_t t0 = claim();
-    tA = claim();
-    tB = claim();
+    if (!GRFC_ALG1_RES1) {
+      tA = claim();
+      tB = claim();
+    }
     publish(t0, 0);
   }
   __syncthreads();
   uint32_t* done_ctr = nullptr;
   for (;;) {
     const Msg m = s_msg;
-    if (threadIdx.x == 0 && tA < total) {
-      const uint32_t* ctr;
-      dep_of(decode(tA), ctr);
-      dep_v = ld_relaxed_u32(ctr);
+    if (threadIdx.x == 0) {
+      if (GRFC_ALG1_RES1) {
+        if (m.t < total) tA = claim();
+      } else if (tA < total) {
+        const uint32_t* ctr;
+        dep_of(decode(tA), ctr);
+        dep_v = ld_relaxed_u32(ctr);
+      }
     }
     if (m.t >= total) break;
     if (!m.ready) {
@@ -313,9 +329,13 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
       done_ctr = &q.row_done[m.slot];
     }
     if (threadIdx.x == 0) {
-      publish(tA, dep_v);
-      tA = tB;
-      tB = tB < total ? claim() : total;
+      if (GRFC_ALG1_RES1) {
+        publish(tA < total ? tA : total, 0);
+      } else {
+        publish(tA, dep_v);
+        tA = tB;
+        tB = tB < total ? claim() : total;
+      }
     }
     __syncthreads();
   }
