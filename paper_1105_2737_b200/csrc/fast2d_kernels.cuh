@@ -146,12 +146,21 @@ constexpr int row_threads() {
 constexpr int hibit(int i) { return i >= 16 ? 16 : i >= 8 ? 8 : i >= 4 ? 4 : i >= 2 ? 2 : 1; }
 
 template <int N, int E, int R, int NS, int SIGN, typename C>
-__device__ __forceinline__ void stage_compute(C* v, int j, const C* __restrict__ tw, int tws) {
+__device__ __forceinline__ void stage_compute(C* v, int j, const C* __restrict__ tw, int tws,
+                                              const C* t16 = nullptr) {
   constexpr int TT = N / E;
 #pragma unroll
   for (int b = 0; b < E / R; ++b) {
     if constexpr (NS > 1) {
       const int k = (j + b * TT) % NS;
+      if constexpr (NS == 16 && R == 16 && SIGN > 0 && sizeof(C) == 8) {
+        if (t16) {  // per-CTA table of e^{2 pi i i k / 256}, row i-1, column k (LDS per twiddle)
+#pragma unroll
+          for (int i = 1; i < R; ++i) v[b * R + i] = cmul(v[b * R + i], t16[(i - 1) * 16 + k]);
+          dft<R, SIGN>(&v[b * R]);
+          continue;
+        }
+      }
       if constexpr (GRFC_TWREC && sizeof(C) == 8 && R >= 4 && R <= 32) {
         C w[R];
         Unroll<1, R>::run([&](auto ii) {
@@ -198,6 +207,9 @@ __device__ __forceinline__ int stage_in_index(int j, int b, int i) {
 // pad(base + off) = pad(base) + pad(off) for every stage: see RowEx).
 template <typename Ex, typename = void>
 struct HasPut2 : std::false_type {};
+#ifndef GRFC_TW16
+#define GRFC_TW16 1
+#endif
 #ifndef GRFC_GEN_NOBAR
 #define GRFC_GEN_NOBAR 1
 #endif
@@ -228,12 +240,25 @@ __device__ __forceinline__ C ex_get(const Ex& ex, int base) {
     return ex.get(base + OFF);
 }
 
+// Optional shared-memory twiddle table carried by an exchange (`tw16` member).
+template <typename Ex, typename = void>
+struct HasTw16 : std::false_type {};
+template <typename Ex>
+struct HasTw16<Ex, std::void_t<decltype(Ex::tw16)>> : std::true_type {};
+template <typename C, typename Ex>
+__device__ __forceinline__ const C* ex_tw16(const Ex& ex) {
+  if constexpr (HasTw16<Ex>::value)
+    return ex.tw16;
+  else
+    return nullptr;
+}
+
 // Runs the stages on v (stage-0 inputs already in v, ordered b*R0 + i).
 // Exchanges go through `ex`. On return v[b*RL + i] holds output element
 // j + b*TT + i*N/RL (RL the last radix).
 template <int N, int E, int SIGN, int NS, int R, int... Rest, typename C, typename Ex>
 __device__ __forceinline__ void run_stages(C* v, int j, const C* __restrict__ tw, int tws, Ex& ex) {
-  stage_compute<N, E, R, NS, SIGN>(v, j, tw, tws);
+  stage_compute<N, E, R, NS, SIGN>(v, j, tw, tws, ex_tw16<C>(ex));
   if constexpr (sizeof...(Rest) > 0) {
     constexpr int R2 = RFirst<Radices<Rest...>>::value;
     constexpr int TT = N / E;
@@ -330,6 +355,7 @@ struct ColExPad {
   C* s;
   int slot;
   LateDep dep{};
+  const C* tw16 = nullptr;  // optional shared twiddle table (stage_compute)
   __device__ __forceinline__ static int row(int e) { return e + (e >> 4); }
   __device__ __forceinline__ void put(int e, C v) { s[row(e) * SLOTS + slot] = v; }
   __device__ __forceinline__ C get(int e) const { return s[row(e) * SLOTS + slot]; }
@@ -372,6 +398,7 @@ struct RowEx {
   C* s;
   bool active = true;  // idle teams (beyond the tile's rows) keep to the barriers only
   int bar = 0;
+  const C* tw16 = nullptr;  // optional shared twiddle table (stage_compute)
   static constexpr int PER = 128 / (int)sizeof(C);
   __host__ __device__ __forceinline__ static constexpr int pad(int e) { return e + e / PER; }
   __device__ __forceinline__ bool on() const { return ALL || active; }
@@ -570,7 +597,8 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
                                          const uint32_t* dep = nullptr, uint32_t dep_target = 0,
-                                         uint32_t* sig = nullptr, Hook hook = Hook{}) {
+                                         uint32_t* sig = nullptr, Hook hook = Hook{},
+                                         const C_t<T>* t16 = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -691,6 +719,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     __syncthreads();
     using Ex = std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
     Ex ex{sm, slot};
+    if constexpr (HasTw16<Ex>::value) ex.tw16 = t16;
     // The slot's previous field must be consumed before W is overwritten: checked
     // at the FFT's exchange barriers (all W stores follow the last one).
     constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
@@ -786,7 +815,7 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
                                          const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
-                                         uint32_t* sig = nullptr, Hook hook = Hook{}) {
+                                         uint32_t* sig = nullptr, Hook hook = Hook{}, const C_t<T>* t16 = nullptr) {
   using C = C_t<T>;
   using PL = RowPlan<M, T>;
   constexpr int E = PL::E, TT = M / E;
@@ -812,7 +841,7 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
   constexpr int TEAMS = (NT > 0 ? NT : RPT * TT) / TT;
   constexpr int NAMED = (GRFC_ROW_NAMED && !WARP && TT % 32 == 0 && TEAMS <= 15) ? TT : 0;
   RowEx<C, ALL, WARP, NAMED> ex{reinterpret_cast<C*>(smem_raw) + (ALL ? rl : (rl < RPT ? rl : 0)) * row_pitch<M, C>(),
-                                ALL || rl < RPT, 1 + rl};
+                                ALL || rl < RPT, 1 + rl, t16};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   C* o = reinterpret_cast<C*>(of + (int64_t)row * (2 * M));
@@ -936,6 +965,19 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   constexpr int RPT = rows_per_tile<N1, M, T>();
   const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
   if (table) fused2d_row_table<N1>(p, s_rowq);
+  // fp32: per-CTA table of the radix-16 stage twiddles e^{2 pi i r k / 256} (r = 1..15,
+  // k < 16), shared by the column and row FFTs' NS = 16 stages (LDS instead of products)
+  __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
+  const C_t<T>* t16 = nullptr;
+  if constexpr (GRFC_TW16 && sizeof(T) == 4) {
+    for (int e = threadIdx.x; e < 240; e += blockDim.x) {
+      double sn, cs;
+      sincospi(2.0 * (double)((e / 16 + 1) * (e % 16)) / 256.0, &sn, &cs);
+      s_tw16[e] = mk<C_t<T>>((T)cs, (T)sn);
+    }
+    __syncthreads();
+    t16 = s_tw16;
+  }
   // One CTA barrier per tile. At the end of tile i thread 0 publishes ticket
   // i+1 (its atomic was issued when tile i started, so the round trip hides
   // behind tile i) together with whether i+1's dependency — its field's
@@ -1095,11 +1137,11 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     if (m.col) {
       col_tile<T, N1, ALG, M>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
                               GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr,
-                              hook);
+                              hook, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
       row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
-                                                     smem_raw, done_ctr, hook);
+                                                     smem_raw, done_ctr, hook, t16);
       done_ctr = &q.row_done[m.slot];
     }
     // every tile has internal barriers, so all threads have read s_msg
