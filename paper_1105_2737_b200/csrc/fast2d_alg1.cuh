@@ -37,7 +37,8 @@ __device__ __forceinline__ C_t<T> half_c(C_t<T> a) {
 template <typename T, int N1, int M, int RPT>
 __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int r0,
                                         C_t<T>* __restrict__ Wf, const C_t<T>* __restrict__ tw2,
-                                        unsigned char* smem_raw, uint32_t* sig = nullptr) {
+                                        unsigned char* smem_raw, uint32_t* sig = nullptr,
+                                        const C_t<T>* t16 = nullptr) {
   using C = C_t<T>;
   using PL = RowPlan<M, T>;
   constexpr int E = PL::E, TT = M / E, H = RPT / 2, PITCH = row_pitch<M, C>();
@@ -70,7 +71,7 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
   __syncthreads();
   // the row's team is a half warp: warp-level exchange (as row_tile)
   constexpr bool WARP = GRFC_ROW_WARPSYNC && TT <= 32 && 32 % TT == 0;
-  RowEx<C, false, WARP> ex{sm + rs * PITCH, live};
+  RowEx<C, false, WARP> ex{sm + rs * PITCH, live, 0, t16};
   line_fft<M, E, +1>(v, j, tw2, 2, ex, typename PL::R{});
   if (!live) return;
   const int row = rl < H ? r0 + rl : r0 + (rl - H) + N1 / 2;
@@ -86,7 +87,7 @@ template <typename T, int N1>
 __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                               const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                               unsigned char* smem_raw,
-                                              uint32_t* sig = nullptr) {
+                                              uint32_t* sig = nullptr, const C_t<T>* t16 = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -129,6 +130,7 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
     }
   __syncthreads();
   std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{sm, slot};
+  if constexpr (HasTw16<decltype(ex)>::value) ex.tw16 = t16;
   // Both column FFTs run through ONE copy of the transform code (a rolled
   // two-pass loop): the kernel's three tile types otherwise overflow the
   // instruction cache (ncu: "no instruction" stalls).
@@ -210,6 +212,8 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
                    const C_t<T>* __restrict__ tw2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RPT = rows_per_tile<N1, M, T>();
+  __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
+  const C_t<T>* t16 = init_tw16<T>(s_tw16);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t L = q.L, F = q.F, g1 = q.g1, gc = q.gc, g2 = q.g2;
   // ticket ranges (L <= F/2): [0,L): R1 | [L,2L): R1 C | [2L,F): R1 C R2 | [F,F+L): C R2 | [F+L,F+2L): R2
@@ -319,13 +323,14 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
     }
     C_t<T>* Wf = ring + m.slot * slot_elems;
     if (m.kind == 0) {
-      r1_tile<T, N1, M, RPT>(p, key, field0 + m.f, (int)m.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr);
+      r1_tile<T, N1, M, RPT>(p, key, field0 + m.f, (int)m.idx * (RPT / 2), Wf, tw2, smem_raw, done_ctr, t16);
       done_ctr = &q.r1_done[m.slot];
     } else if (m.kind == 1) {
-      alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, done_ctr);
+      alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, done_ctr, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2, smem_raw, done_ctr);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
+                                                     smem_raw, done_ctr, NoHook{}, t16);
       done_ctr = &q.row_done[m.slot];
     }
     if (threadIdx.x == 0) {

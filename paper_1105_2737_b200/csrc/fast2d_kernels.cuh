@@ -585,6 +585,23 @@ __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* _
                                              const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
                                              int col, bool packed, bool mid);
 
+// Fills the per-CTA radix-16 twiddle table (fp32; see stage_compute) and returns
+// it (nullptr for fp64). Ends with a CTA barrier.
+template <typename T>
+__device__ __forceinline__ const C_t<T>* init_tw16(C_t<T>* tab) {
+  if constexpr (GRFC_TW16 && sizeof(T) == 4) {
+    for (int e = threadIdx.x; e < 240; e += blockDim.x) {
+      double sn, cs;
+      sincospi(2.0 * (double)((e / 16 + 1) * (e % 16)) / 256.0, &sn, &cs);
+      tab[e] = mk<C_t<T>>((T)cs, (T)sn);
+    }
+    __syncthreads();
+    return tab;
+  } else {
+    return nullptr;
+  }
+}
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -968,16 +985,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   // fp32: per-CTA table of the radix-16 stage twiddles e^{2 pi i r k / 256} (r = 1..15,
   // k < 16), shared by the column and row FFTs' NS = 16 stages (LDS instead of products)
   __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
-  const C_t<T>* t16 = nullptr;
-  if constexpr (GRFC_TW16 && sizeof(T) == 4) {
-    for (int e = threadIdx.x; e < 240; e += blockDim.x) {
-      double sn, cs;
-      sincospi(2.0 * (double)((e / 16 + 1) * (e % 16)) / 256.0, &sn, &cs);
-      s_tw16[e] = mk<C_t<T>>((T)cs, (T)sn);
-    }
-    __syncthreads();
-    t16 = s_tw16;
-  }
+  const C_t<T>* t16 = init_tw16<T>(s_tw16);
   // One CTA barrier per tile. At the end of tile i thread 0 publishes ticket
   // i+1 (its atomic was issued when tile i started, so the round trip hides
   // behind tile i) together with whether i+1's dependency — its field's

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T
 template <typename T, int N1>
 __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int j0l, int n0_per, int n1_per, int m,
                                              int s, C_t<T>* __restrict__ dst, const C_t<T>* __restrict__ tw1,
-                                             unsigned char* smem_raw) {
+                                             unsigned char* smem_raw, const C_t<T>* t16 = nullptr) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, SLOTS = 2 * PL::X, TT = N1 / E;
@@ -271,6 +271,7 @@ __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int
       v[b * R0 + i] = __ldcs(&src[(((int64_t)r * n0_per + j0l) * n1_per + k1l) * m + col]);
     }
   std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{reinterpret_cast<C*>(smem_raw), slot};
+  if constexpr (HasTw16<decltype(ex)>::value) ex.tw16 = t16;
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
@@ -292,6 +293,8 @@ __global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_ticket;
   constexpr int RPT = rows_per_tile<N1, M, T>();
+  __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
+  const C_t<T>* t16 = init_tw16<T>(s_tw16);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
   const uint32_t total = q.F * G;
@@ -326,11 +329,12 @@ __global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1,
     C_t<T>* Wp = ring + slot * slot_elems;
     if (col) {
       wait_geq(&q.row_done[slot], use * q.rtiles);
-      c2c_col_tile<T, N1>(src, (int)f, n0_per, n1_per, M, (int)idx, Wp, tw1, smem_raw);
+      c2c_col_tile<T, N1>(src, (int)f, n0_per, n1_per, M, (int)idx, Wp, tw1, smem_raw, t16);
       signal_done(&q.col_done[slot]);
     } else {
       wait_geq(&q.col_done[slot], (use + 1) * q.strips);
-      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw,
+                                                     nullptr, NoHook{}, t16);
       signal_done(&q.row_done[slot]);
     }
   }
