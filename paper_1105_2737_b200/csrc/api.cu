@@ -423,7 +423,10 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
                            cudaMemcpyHostToDevice));
     }
   }
-  if (density->family == GRFC_DENSITY_TABLE) GRFC_CUDA(cudaMalloc(&p->d_table, p->cells * sizeof(double)));
+  if (density->family == GRFC_DENSITY_TABLE) {
+    GRFC_CUDA(cudaMalloc(&p->d_table, p->cells * sizeof(double)));
+    GRFC_CUDA(cudaMemset(p->d_table, 0, p->cells * sizeof(double)));
+  }
   // Fused fast path for power-of-two 2D shapes (pow2_2d.cu).
   // GRFC_DISABLE_FAST=1 forces the generic kernels (A/B parity testing).
   const char* nofast = std::getenv("GRFC_DISABLE_FAST");
@@ -454,7 +457,10 @@ grfc_status grfc_plan_set_sqrt_gamma_table(grfc_plan p, const double* sg) {
   DeviceGuard guard(p->device);
   GRFC_CUDA(cudaMemcpy(p->d_table, sg, p->cells * sizeof(double), cudaMemcpyHostToDevice));
   p->D.table = p->d_table;
-  if (p->fast) p->fast2d.D.table = p->d_table;
+  if (p->fast) {
+    const cudaError_t e = fast2d_set_table(p->fast2d, p->d_table);
+    if (e != cudaSuccess) return fail(GRFC_ECUDA, std::string("CUDA: density table: ") + cudaGetErrorString(e));
+  }
   if (p->fast3) p->fast3d.D.table = p->d_table;
   p->table_set = true;
   return GRFC_OK;

@@ -24,12 +24,16 @@ struct Fast2D {
   // fp32 Algorithm 2: sqrt(g) x scale / sqrt 2 per half-lattice cell (n1 x (n2/2+1)),
   // evaluated once per plan in fp64; nullptr when larger than kSgTableMax
   float* d_sg = nullptr;
+  double sg_mult = 1.0;  // the factor d_sg folds in
   static constexpr size_t kSgTableMax = 8u << 20;
   int kind = 0;
   // persistent fused kernel geometry (fused_query)
   bool persistent = false;
   bool warp = false;  // warp-synchronous column tiles + transposed W (fast2d_warp.cuh)
   int occ = 1, sms = 148, strips = 0, rtiles = 0;
+  // cluster-scheduled fused kernel (k_fused2d_cl): CTAs per cluster (0 = off),
+  // W slots per cluster, resident clusters
+  int cluster = 0, cslots = 1, nclusters = 0;
   // two-stream pipeline: column kernels on sa, row kernels on sb, a ring of
   // kRing chunk slots ordered by events (no in-kernel waiting).
   static constexpr int kRing = 3;
@@ -76,6 +80,8 @@ bool fast2d_supported(int d, const int64_t* n, int dtype, int alg, int family);
 cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int dtype, int alg, double s_one,
                         double s_two);
 void fast2d_free(Fast2D& f);
+// (Re)builds the fp32 density table d_sg from the user's sqrt(g) table (GRFC_DENSITY_TABLE).
+cudaError_t fast2d_set_table(Fast2D& f, const double* d_table);
 const char* fast2d_name(const Fast2D& f);
 // W: workspace of nf * |H| complex; out + i*stride (elements) = field i.
 cudaError_t launch_fast2d(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,

@@ -16,6 +16,8 @@
 //   R2  rows: row_tile (M-point exp(+) FFT -> the field rows), as Algorithm 2.
 #pragma once
 
+#include <atomic>
+
 #include "fast2d_kernels.cuh"
 
 namespace grfc {
@@ -255,8 +257,11 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
     if (x.kind == 1) return ctr = &q.r1_done[x.slot], (x.use + 1) * g1;
     return ctr = &q.col_done[x.slot], (x.use + 1) * gc;
   };
-  // Same schedule as k_fused2d: one barrier per tile, two reserved tickets,
-  // early relaxed dependency loads, completion released inside the next tile.
+  // Schedule of k_fused2d: one barrier per tile, completion released inside the
+  // next tile. Default (GRFC_ALG1_RES1=1): one reserved ticket, claimed at the top
+  // of a tile and checked in publish() at its end with an acquire load (exposed
+  // round trip; k_fused2d hides it with a mid-tile hook). GRFC_ALG1_RES1=0: two
+  // reserved tickets with early relaxed dependency loads.
   uint32_t tA = total, tB = total, dep_v = 0;
   auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
   // thread 0 decodes (integer divisions) and publishes the next tile
@@ -373,11 +378,17 @@ cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, i
   using C = C_t<T>;
   constexpr int NT = fused_threads<N1, M, T>(), RPT = rows_per_tile<N1, M, T>();
   constexpr size_t smem = fused_smem<N1, M, T>();
-  static int occ = 0;
+  // the smem attribute is per device: set on every launch (cheap); the occupancy
+  // is cached per device ordinal
+  static std::atomic<int> occ_cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaFuncSetAttribute(k_fused2d_alg1<T, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = dev < 64 ? occ_cache[dev].load(std::memory_order_relaxed) : 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_fused2d_alg1<T, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d_alg1<T, N1, M>, NT, smem);
     if (occ < 1) occ = 1;
+    if (dev < 64) occ_cache[dev].store(occ, std::memory_order_relaxed);
   }
   F2Sched3 q{};
   uint32_t conc = 0;

@@ -15,7 +15,10 @@ template cudaError_t launch_rows<INST_T, INST_N / 2>(const Fast2D&, int64_t, con
 #define GRFC_FUSED(M)                                                                                    \
   template cudaError_t launch_fused<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(                                \
       const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*, int64_t, cudaStream_t);                        \
-  template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(Fast2D&);
+  template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(Fast2D&);                         \
+  template cudaError_t launch_cluster<INST_T, INST_N, M>(const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*,   \
+                                                         int64_t, cudaStream_t);                                    \
+  template cudaError_t cluster_query<INST_T, INST_N, M>(Fast2D&, int, int);
 GRFC_FUSED(128)
 GRFC_FUSED(256)
 GRFC_FUSED(512)

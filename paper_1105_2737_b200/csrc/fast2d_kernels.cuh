@@ -609,13 +609,15 @@ struct NoHook {
 // `hook` runs on thread 0 once per tile, mid-tile (after the generation barrier
 // of a column tile, behind the W loads of a row tile): the persistent
 // scheduler checks the next tile's dependency there, off the critical path.
-template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook>
+// `pre` runs on every thread after the column FFT and before the W stores (the
+// cluster scheduler waits there for the W slot to be free).
+template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
                                          const uint32_t* dep = nullptr, uint32_t dep_target = 0,
                                          uint32_t* sig = nullptr, Hook hook = Hook{},
-                                         const C_t<T>* t16 = nullptr) {
+                                         const C_t<T>* t16 = nullptr, Pre pre = Pre{}) {
   using C = C_t<T>;
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
@@ -731,6 +733,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll
       for (int i = 0; i < RL; ++i) rg[RowEx<C>::pad(j + b * TT + i * (N1 / RL))] = v[b * RL + i];
     LateDep{dep, dep_target, dep_seen, 0}.check();
+    pre();
     __syncthreads();
   } else {
     __syncthreads();
@@ -742,6 +745,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
     if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
     line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    pre();
     if (dep && !has_ex) {
       if (threadIdx.x == 0 && dep_seen < dep_target)
         while (ld_relaxed_u32(dep) < dep_target) __nanosleep(256);
@@ -1183,6 +1187,99 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   }
 }
 
+// ---------------------------------------------------------------- cluster-scheduled fused kernel
+// One launch per batch, persistent, launched as thread-block clusters of CS
+// CTAs. Cluster c owns fields c, c + nclusters, ...; CTA rank r of the cluster
+// runs column strips r, r + CS, ... and row tiles r, r + CS, ... of each of
+// them. The field's half-spectrum W lives in the cluster's own slot(s) of the
+// workspace (nclusters x NSL x P*s bytes — sized to stay L2-resident), and the
+// hand-offs are cluster barriers (barrier.cluster arrive.release /
+// wait.acquire: ~400 cycles, no global atomics, no polling):
+//   NSL = 1: C(f) | arrive, wait | R(f) | arrive | [C(f+1) computes] wait | stores
+//   NSL = 2: C(f) -> slot f%2 | arrive, wait | R(f) | C(f+1) -> slot (f+1)%2
+//            (passing the barrier after C(f) implies every CTA finished R(f-1),
+//             the last reader of slot (f+1)%2)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t ncluster_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+struct ClusterWaitPre {
+  bool on;
+  __device__ __forceinline__ void operator()() const {
+    if (on) cluster_wait();
+  }
+};
+
+#ifndef GRFC_CL_MINB
+#define GRFC_CL_MINB 4
+#endif
+template <int N1, int M, typename T>
+constexpr int cl_min_blocks() {
+  return (N1 == 512 && sizeof(T) == 4) ? GRFC_CL_MINB : fused_min_blocks<N1, M, T>();
+}
+template <typename T, int N1, int M, int NSL>
+__global__ void __launch_bounds__(fused_threads<N1, M, T>(), cl_min_blocks<N1, M, T>())
+    k_fused2d_cl(F2Params p, PhiloxKey key, uint64_t field0, uint32_t F, C_t<T>* __restrict__ ws, T* __restrict__ out,
+                 int64_t out_stride, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ float s_rowq[N1];
+  constexpr int RPT = rows_per_tile<N1, M, T>();
+  constexpr uint32_t STRIPS = M / (2 * ColPlan<N1, T>::X), RT = N1 / RPT;
+  constexpr int NT = fused_threads<N1, M, T>();
+  const bool table = sizeof(T) == 4 && (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV);
+  if (table) fused2d_row_table<N1>(p, s_rowq);
+  __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
+  const C_t<T>* t16 = init_tw16<T>(s_tw16);
+  const uint32_t rank = cluster_ctarank(), cs = cluster_nctarank();
+  const uint32_t cid = cluster_id_x(), ncl = ncluster_x();
+  const uint64_t slot_elems = (uint64_t)N1 * M;
+  C_t<T>* const wbase = ws + (uint64_t)cid * NSL * slot_elems;
+  uint32_t it = 0;
+  for (uint32_t f = cid; f < F; f += ncl, ++it) {
+    C_t<T>* Wf = wbase + (NSL == 2 ? (it & 1u) : 0u) * slot_elems;
+    bool first = true;
+    for (uint32_t sidx = rank; sidx < STRIPS; sidx += cs) {
+      // NSL = 1: the slot is free once every CTA of the cluster finished R(f-1)
+      // (the arrive after its rows); the first column tile waits for that just
+      // before its W stores, so the barrier's latency hides behind its FFT.
+      const ClusterWaitPre pre{NSL == 1 && first && it > 0};
+      col_tile<T, N1, GRFC_ONE_FFT_OVERWRITE, M, NoHook, ClusterWaitPre>(
+          p, key, field0 + f, (int)sidx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, nullptr, 0, nullptr,
+          NoHook{}, t16, pre);
+      first = false;
+      __syncthreads();
+    }
+    if (NSL == 1 && first && it > 0) cluster_wait();  // no column tile on this rank
+    cluster_arrive();
+    cluster_wait();
+    for (uint32_t r = rank; r < RT; r += cs) {
+      row_tile<T, M, RPT, NT>(Wf, (int)r * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw, nullptr, NoHook{},
+                              t16);
+      __syncthreads();
+    }
+    if (NSL == 1) cluster_arrive();
+  }
+  if (NSL == 1 && it > 0) cluster_wait();  // pair the last arrive
+}
+
 // Two-kernel variant (A/B and fallback): all column tiles of a chunk, then
 // all its row tiles.
 template <typename T, int N1, int ALG>
@@ -1248,11 +1345,8 @@ cudaError_t launch_cols(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t
   constexpr int CB = ColPlan<N1, T>::X;
   const size_t smem = col_warp_mode<N1, T>() ? (size_t)wcol_pitch(N1) * 2 * CB * sizeof(C)
                                              : (size_t)(col_padded<N1, T>() ? colx_rows(N1) : N1) * 2 * CB * sizeof(C);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_cols_gen<T, N1, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // set on every launch: the attribute is per device (a process may use several)
+  cudaFuncSetAttribute(k_cols_gen<T, N1, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int strips = (f.n2 / 2) / (2 * CB);
   const C* tw1 = (const C*)f.d_tw;
   const C* tw2 = tw1 + f.n1;
@@ -1268,11 +1362,8 @@ cudaError_t launch_rows(const Fast2D& f, int64_t nf, const void* W, void* out, i
   using C = C_t<T>;
   constexpr int RPB = RowPlan<M, T>::X;
   const size_t smem = (size_t)RPB * row_pitch<M, C>() * sizeof(C);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_rows_c2r<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // set on every launch: the attribute is per device (a process may use several)
+  cudaFuncSetAttribute(k_rows_c2r<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t rows = nf * f.n1;
   const C* tw2 = (const C*)f.d_tw + f.n1;
   LaunchScope ls("fused_rows_c2r", s);
@@ -1349,6 +1440,70 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
                  grid, q.L, q.S, h[5], h[0] / nc, h[2] / nc, h[6], h[1] / nr, h[3] / nr, h[4] / (nc + nr));
   }
   return e;
+}
+
+template <typename T, int N1, int M>
+cudaError_t cluster_query(Fast2D& f, int cs, int nsl) {
+  constexpr int NT = fused_threads<N1, M, T>();
+  constexpr size_t smem = fused_smem<N1, M, T>();
+  const void* fn = nsl == 2 ? (const void*)k_fused2d_cl<T, N1, M, 2> : (const void*)k_fused2d_cl<T, N1, M, 1>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)cs, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
+  if (e != cudaSuccess) return e;
+  if (ncl < 1) return cudaErrorInvalidConfiguration;
+  f.cluster = cs;
+  f.cslots = nsl;
+  f.nclusters = ncl;
+  if (std::getenv("GRFC_CL_DEBUG"))
+    std::fprintf(stderr, "[grfc cluster] size %d slots %d active clusters %d (%d CTAs of %d threads, smem %zu)\n", cs,
+                 nsl, ncl, ncl * cs, NT, smem);
+  return cudaSuccess;
+}
+
+template <typename T, int N1, int M>
+cudaError_t launch_cluster(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
+                           int64_t stride, cudaStream_t s) {
+  using C = C_t<T>;
+  constexpr int NT = fused_threads<N1, M, T>();
+  constexpr size_t smem = fused_smem<N1, M, T>();
+  const uint32_t ncl = (uint32_t)std::min<int64_t>(f.nclusters, nf);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)f.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(ncl * (unsigned)f.cluster, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const C* tw1 = (const C*)f.d_tw;
+  const C* tw2 = tw1 + f.n1;
+  LaunchScope ls("fused2d_cluster", s);
+  if (f.cslots == 2)
+    return cudaLaunchKernelEx(&cfg, k_fused2d_cl<T, N1, M, 2>, make_params(f), philox_key(seed), field0, (uint32_t)nf,
+                              (C*)ws, (T*)out, stride, tw1, tw2);
+  return cudaLaunchKernelEx(&cfg, k_fused2d_cl<T, N1, M, 1>, make_params(f), philox_key(seed), field0, (uint32_t)nf,
+                            (C*)ws, (T*)out, stride, tw1, tw2);
 }
 
 }  // namespace grfc

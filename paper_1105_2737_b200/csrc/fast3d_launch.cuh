@@ -46,11 +46,8 @@ cudaError_t launch_3d_colgen(const Fast3D& f, uint64_t seed, uint64_t field, voi
   using C = C_t<T>;
   constexpr int CB = ColPlan3<N0, T>::X, SLOTS = 4 * CB;
   const size_t smem = (size_t)N0 * (SLOTS + 2) * sizeof(C);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_3d_colgen<T, N0, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // set on every launch: the attribute is per device (a process may use several)
+  cudaFuncSetAttribute(k_3d_colgen<T, N0, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int strips = (f.n2 / 2) / (2 * CB);
   const unsigned blocks = (unsigned)((f.n1 / 2 + 1) * strips);
   const C* tw0 = (const C*)f.d_tw;

@@ -27,6 +27,11 @@ cudaError_t launch_fusedw(const Fast2D& f, uint64_t seed, uint64_t field0, int64
 template <typename T, int N1, int M>
 cudaError_t fusedw_query(Fast2D& f);
 template <typename T, int N1, int M>
+cudaError_t launch_cluster(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
+                           int64_t stride, cudaStream_t s);
+template <typename T, int N1, int M>
+cudaError_t cluster_query(Fast2D& f, int cs, int nsl);
+template <typename T, int N1, int M>
 cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out, int64_t stride,
                               cudaStream_t s);
 
@@ -130,6 +135,18 @@ static cudaError_t dispatch_query(Fast2D& f) {
   GRFC_DISPATCH_N1(T, ALG, GRFC_CALL_QUERY)
 }
 
+#define GRFC_CALL_CL(T, N1, M, ALG) launch_cluster<T, N1, M>(f, seed, field0, nf, W, out, stride, s)
+#define GRFC_CALL_CLQ(T, N1, M, ALG) cluster_query<T, N1, M>(f, cs, nsl)
+template <typename T>
+static cudaError_t dispatch_cluster(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
+                                    int64_t stride, cudaStream_t s) {
+  GRFC_DISPATCH_N1(T, 0, GRFC_CALL_CL)
+}
+template <typename T>
+static cudaError_t dispatch_clquery(Fast2D& f, int cs, int nsl) {
+  GRFC_DISPATCH_N1(T, 0, GRFC_CALL_CLQ)
+}
+
 #define GRFC_CALL_WQ(T, N1, M, ALG) fusedw_query<T, N1, M>(f)
 #define GRFC_CALL_W(T, N1, M, ALG) launch_fusedw<T, N1, M>(f, seed, field0, nf, W, out, stride, s)
 #define GRFC_DISPATCH_N1W(T, CALL)                       \
@@ -153,6 +170,8 @@ static cudaError_t dispatch_w(const Fast2D& f, uint64_t seed, uint64_t field0, i
 template <typename T>
 static cudaError_t run_fast(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                             int64_t stride, cudaStream_t s) {
+  if (f.persistent && f.cluster && alg == GRFC_ONE_FFT_OVERWRITE)
+    return dispatch_cluster<T>(f, seed, field0, nf, W, out, stride, s);
   if (f.persistent && alg == GRFC_ONE_FFT_OVERWRITE)
     return f.warp ? dispatch_w<T>(f, seed, field0, nf, W, out, stride, s)
                   : dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s);
@@ -172,6 +191,14 @@ __global__ void k_sg_table(GridDesc g, DensityDesc D, double mult, float* __rest
     wrap_freq(g, k, kw);
     out[h] = (float)(sqrt_gamma<double>(g, D, kw, h) * mult);
   }
+}
+
+cudaError_t fast2d_set_table(Fast2D& f, const double* d_table) {
+  if (d_table) f.D.table = d_table;
+  if (!f.d_sg) return cudaSuccess;
+  k_sg_table<<<148, 256>>>(f.g, f.D, f.sg_mult, f.d_sg);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? cudaDeviceSynchronize() : e;
 }
 
 cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int dtype, int alg, double s_one,
@@ -216,10 +243,13 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
     f.fail_what = "density table";
     e = cudaMalloc(&f.d_sg, sg_bytes);
     if (e != cudaSuccess) return e;
-    k_sg_table<<<148, 256>>>(g, D, alg1_f32 ? s_two : s_one * 0.70710678118654752440, f.d_sg);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return e;
+    f.sg_mult = alg1_f32 ? s_two : s_one * 0.70710678118654752440;
+    // a user table (GRFC_DENSITY_TABLE) is not uploaded yet: fast2d_set_table
+    // builds d_sg when grfc_plan_set_sqrt_gamma_table supplies it
+    if (D.family != GRFC_DENSITY_TABLE) {
+      e = fast2d_set_table(f, nullptr);
+      if (e != cudaSuccess) return e;
+    }
   }
   // Pipeline chunk: ~12 MiB of half-spectrum per slot, 3 slots in flight (L2-resident).
   const double slot = (double)f.n1 * (f.n2 / 2) * cs;
@@ -253,12 +283,24 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
     return dtype == GRFC_F64 ? dispatch_wquery<double>(f) : dispatch_wquery<float>(f);
   e = dtype == GRFC_F64 ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
                         : dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f);
+  if (e != cudaSuccess) return e;
+  // Cluster-scheduled variant (k_fused2d_cl): GRFC_CLUSTER = CTAs per cluster,
+  // GRFC_CSLOTS = W slots per cluster (1 or 2).
+  const char* ce = std::getenv("GRFC_CLUSTER");
+  const int ncs = ce ? std::atoi(ce) : 0;
+  if (ncs > 0) {
+    const char* se = std::getenv("GRFC_CSLOTS");
+    const int nsl = se && se[0] == '2' ? 2 : 1;
+    f.fail_what = "cluster kernel query";
+    e = dtype == GRFC_F64 ? dispatch_clquery<double>(f, ncs, nsl) : dispatch_clquery<float>(f, ncs, nsl);
+  }
   return e;
 }
 
 size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf) {
   const size_t slot = (size_t)f.n1 * (size_t)(f.n2 / 2) * (f.dtype == GRFC_F64 ? 16 : 8);
   if (!f.persistent) return slot * (size_t)nf;
+  if (f.cluster) return slot * (size_t)f.cslots * (size_t)std::min<int64_t>(f.nclusters, nf);
   uint32_t L, S, c;
   fused_geometry(f, nf, &L, &S, &c);
   return fused_ctr_bytes(S) + slot * S;

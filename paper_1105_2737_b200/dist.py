@@ -75,7 +75,14 @@ def estimate_covariance_distributed(plan: Optional["grfc.Plan"], seed: int, samp
         return merge_fn(mine, samples)
     # pad every rank's stack to the largest count, gather, drop the padding in rank order
     maxc = chunk_range(0, world, samples)[1]
-    dev = mine.device if mine is not None else torch.device("cpu")
+    # a rank that owns no chunks still joins the all_gather with a buffer on the
+    # backend's device (NCCL: this rank's GPU; mixing CPU and CUDA buffers hangs)
+    if mine is not None:
+        dev = mine.device
+    elif dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = torch.device("cpu")
     buf = torch.zeros((maxc, P), dtype=torch.float64, device=dev)
     if count:
         buf[:count] = mine

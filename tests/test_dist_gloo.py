@@ -11,6 +11,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -25,20 +26,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _fields():
+def _fields(samples=SAMPLES):
     from oracle import pyoracle as po
 
     port = po.Port()
     dens = po.density("matern", 2, nu=1.5, ell=0.3)
     n = port.count_draws(COUNTS, po.ONE_FFT_OVERWRITE)
-    draws = np.random.default_rng(11).standard_normal((SAMPLES, n))
+    draws = np.random.default_rng(11).standard_normal((samples, n))
     return np.stack([port.synthesize(COUNTS, LENGTHS, dens, po.ONE_FFT_OVERWRITE, d)[0].ravel() for d in draws])
 
 
 def _partials(fields, c0, n, chunk=1024):
     out = np.zeros((n, fields.shape[1]))
     for k in range(n):
-        for j in range((c0 + k) * chunk, min((c0 + k + 1) * chunk, SAMPLES)):
+        for j in range((c0 + k) * chunk, min((c0 + k + 1) * chunk, fields.shape[0])):
             out[k] = out[k] + fields[j, REF] * fields[j]
     return torch.from_numpy(out)
 
@@ -49,37 +50,41 @@ def _merge(parts, m):
     return torch.from_numpy(gd.kahan_merge_numpy(parts.numpy(), m))
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, samples):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1105_2737_b200 import dist as gd
 
-    fields = _fields()
-    est = gd.estimate_covariance_distributed(None, 0, SAMPLES, REF, partials_fn=lambda c0, n: _partials(fields, c0, n),
+    fields = _fields(samples)
+    est = gd.estimate_covariance_distributed(None, 0, samples, REF, partials_fn=lambda c0, n: _partials(fields, c0, n),
                                              merge_fn=_merge, points=fields.shape[1])
     q.put((rank, est.numpy()))
     dist.destroy_process_group()
 
 
-def test_covariance_partials_world2_bit_identical():
+@pytest.mark.parametrize("samples", [SAMPLES, 1000])
+def test_covariance_partials_world2_bit_identical(samples):
+    """2600 samples: 3 chunks over 2 ranks; 1000 samples: one chunk, so rank 1
+    owns none and joins the all_gather with padding only."""
     from paper_1105_2737_b200 import dist as gd
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     world, port = 2, _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, samples)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=180) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    fields = _fields()
-    single = gd.kahan_merge_numpy(_partials(fields, 0, 3).numpy(), SAMPLES)
+    fields = _fields(samples)
+    nch = (samples + 1023) // 1024
+    single = gd.kahan_merge_numpy(_partials(fields, 0, nch).numpy(), samples)
     for r in range(world):
         assert np.array_equal(got[r], single)  # bitwise, on every rank
     # and the estimate is the plain covariance sum up to rounding
-    direct = (fields[:, REF:REF + 1] * fields).sum(0) / SAMPLES
+    direct = (fields[:, REF:REF + 1] * fields).sum(0) / samples
     assert np.abs(single - direct).max() < 1e-12 * np.abs(direct).max()
 
 
