@@ -166,6 +166,16 @@ grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, dou
 grfc_status grfc_dft_c2c_host(int dim, const int64_t* counts, const double* h_in, double* h_out, int sign,
                               int device);
 
+/* Direct-sum complex DFT, O(P^2), same conventions and errors as grfc_dft_c2c:
+ * the drop-in's NaiveDftBackend (replaces NaiveDftBackend::forward/inverse,
+ * src/dft.cpp:113-165 — the reference's cross-check backend for small grids).
+ * Device pointers, synchronous on `stream`. */
+grfc_status grfc_dft_naive_c2c(int dim, const int64_t* counts, const double* d_in, double* d_out, int sign,
+                               void* stream);
+/* Same with host buffers on `device` (synchronous). */
+grfc_status grfc_dft_naive_c2c_host(int dim, const int64_t* counts, const double* h_in, double* h_out, int sign,
+                                    int device);
+
 /* Slab decomposition of one 3D field over `world` ranks (pow2 3D plans;
  * world divides N0 and N1) — the multi-GPU form of grfc_generate for a
  * single large field. Per field and rank:

@@ -193,6 +193,14 @@ class Reference(_Lib):
                                                   C.byref(res), C.byref(used)))
         return out.reshape(counts), res.value, int(used.value)
 
+    def xoshiro(self, seed, substream, n):
+        """n normals and n raw u64 words of the reference's Xoshiro256Stream(seed, substream)."""
+        normals = np.zeros(n)
+        words = np.zeros(n, np.uint64)
+        self._check(self.lib.ref_xoshiro(C.c_uint64(seed), C.c_uint64(substream), C.c_uint64(n), _ptr(normals),
+                                         _ptr(words, C.c_uint64)))
+        return normals, words
+
     def synthesize_seed(self, counts, lengths, dens, alg, seed):
         out = np.zeros(int(np.prod(counts)))
         self._check(self.lib.ref_synthesize_seed(len(counts), _i64(counts), _f64(lengths), C.byref(dens), alg,

@@ -193,6 +193,17 @@ int ref_synthesize_seed(int dim, const int64_t* counts, const double* lengths, c
   });
 }
 
+// The reference's seeded stream itself: n normals of Xoshiro256Stream(seed,
+// substream) and, from a second instance, n raw next_u64 words (pins the
+// drop-in's bit-identical restatement of random.cpp:56-108).
+int ref_xoshiro(uint64_t seed, uint64_t substream, uint64_t n, double* normals, uint64_t* words) {
+  return guarded([&] {
+    grf::Xoshiro256Stream a(seed, substream), b(seed, substream);
+    for (uint64_t i = 0; i < n; ++i) normals[i] = a.next();
+    for (uint64_t i = 0; i < n; ++i) words[i] = b.next_u64();
+  });
+}
+
 // Full-lattice spectrum (interleaved re/im) from injected draws.
 int ref_spectrum(int dim, const int64_t* counts, const double* lengths, const ref_density* d,
                  int mode, const double* draws, uint64_t ndraws, double* out) {

@@ -6,8 +6,10 @@
 #include <complex>
 #include <cstdint>
 #include <functional>
+#include <span>
 #include <vector>
 
+#include "grf/aligned.hpp"
 #include "grf/grid.hpp"
 #include "grf/random.hpp"
 #include "grf/spectral.hpp"
@@ -26,7 +28,7 @@ void for_each_conjugate_rep(const GridSpec& grid, const std::function<void(const
 
 struct HermitianSpectrum {
   GridSpec grid;
-  std::vector<std::complex<double>> values;  // P entries, row-major
+  aligned_vector<std::complex<double>> values;  // P entries, row-major (hermitian.hpp:48)
 };
 
 enum class SpectrumMode { exact_set, overwrite };
@@ -34,6 +36,10 @@ enum class SpectrumMode { exact_set, overwrite };
 /// V(K) = sqrt(g(w_K)) w(K) on the full lattice from draws pulled from rng.
 HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
                                       SpectrumMode mode);
+/// Allocation-free form (reference hermitian.hpp:66-70): writes all P entries
+/// of out; std::invalid_argument when out.size() != P.
+void synthesize_spectrum_into(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
+                              SpectrumMode mode, std::span<std::complex<double>> out);
 bool verify_hermitian(const HermitianSpectrum& spectrum);
 std::uint64_t spectrum_draw_count(const GridSpec& grid, SpectrumMode mode);
 

@@ -3,7 +3,9 @@
 // reference throws them), RAII plans and density descriptors.
 #pragma once
 
+#include <list>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -35,7 +37,12 @@ grfc_density describe(const SpectralDensity& density);
 /// Throws std::runtime_error on NaN / negative values.
 std::vector<double> sqrt_gamma_table(const GridSpec& grid, const SpectralDensity& density);
 
+using SharedPlan = std::shared_ptr<grfc_plan_s>;
+
 /// fp64 plan for (grid, density, algorithm); the table is filled when needed.
-PlanPtr make_plan(const GridSpec& grid, const SpectralDensity& density, int algorithm, int dtype = GRFC_F64);
+/// Plans of in-kernel density families come from a process-wide LRU cache.
+SharedPlan make_plan(const GridSpec& grid, const SpectralDensity& density, int algorithm, int dtype = GRFC_F64);
+std::mutex& plan_cache_mutex();
+std::list<std::pair<std::string, SharedPlan>>& plan_cache();
 
 }  // namespace grf::detail

@@ -36,9 +36,11 @@ std::uint64_t spectrum_draw_count(const GridSpec& grid, SpectrumMode mode) {
   return n;
 }
 
-HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
-                                      SpectrumMode mode) {
+void synthesize_spectrum_into(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
+                              SpectrumMode mode, std::span<std::complex<double>> out) {
   if (density.dim() != grid.dim()) throw std::invalid_argument("synthesize_spectrum: density dimension mismatch");
+  if (out.size() != static_cast<std::size_t>(grid.point_count()))
+    throw std::invalid_argument("synthesize_spectrum: buffer size does not match grid");
   const int alg = mode == SpectrumMode::overwrite ? GRFC_ONE_FFT_OVERWRITE : GRFC_ONE_FFT_RECURSIVE;
   std::vector<double> draws(spectrum_draw_count(grid, mode));
   for (double& v : draws) v = rng.next();
@@ -49,7 +51,6 @@ HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensit
   const int d = grid.dim();
   const auto& n = grid.counts();
   const std::int64_t hd = n[d - 1] / 2 + 1;
-  HermitianSpectrum out{grid, std::vector<std::complex<double>>(static_cast<std::size_t>(grid.point_count()))};
   // H cells directly; the rest by V(-K) = conj V(K).
   for (std::int64_t lin = 0; lin < grid.point_count(); ++lin) {
     MultiIndex k = grid.index_at(lin);
@@ -63,8 +64,14 @@ HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensit
     h = h * hd + k[d - 1];
     const double g = sg[static_cast<std::size_t>(h)];
     const std::complex<double> v(g * w[2 * h], g * w[2 * h + 1]);
-    out.values[static_cast<std::size_t>(lin)] = conj ? std::conj(v) : v;
+    out[static_cast<std::size_t>(lin)] = conj ? std::conj(v) : v;
   }
+}
+
+HermitianSpectrum synthesize_spectrum(const GridSpec& grid, const SpectralDensity& density, GaussianStream& rng,
+                                      SpectrumMode mode) {
+  HermitianSpectrum out{grid, aligned_vector<std::complex<double>>(static_cast<std::size_t>(grid.point_count()))};
+  synthesize_spectrum_into(grid, density, rng, mode, out.values);
   return out;
 }
 

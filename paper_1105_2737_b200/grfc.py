@@ -111,6 +111,8 @@ def _load():
         "grfc_kernel_timing_read": [C.c_int, P, P, P],
         "grfc_generate_injected_host": [P, P, C.c_uint64, P],
         "grfc_dft_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
+        "grfc_dft_naive_c2c": [C.c_int, P, P, P, C.c_int, P],
+        "grfc_dft_naive_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_conjugate_reps": [C.c_int, P, P, P, C.c_uint64, P],
         "grfc_slab_sizes": [P, C.c_int, P, P, P],
         "grfc_slab_pass_a": [P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, P, P],
@@ -148,6 +150,7 @@ EXPORTED = (
     "grfc_slab_pass_a", "grfc_slab_pass_b", "grfc_estimate_covariance", "grfc_estimate_covariance_host",
     "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
     "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1", "grfc_measure_fp32_peak",
+    "grfc_dft_naive_c2c", "grfc_dft_naive_c2c_host",
 )
 
 
@@ -271,6 +274,12 @@ def half_noise_from_draws(counts: Sequence[int], algorithm: int, draws: np.ndarr
 
 def last_launch_count() -> int:
     return int(_lib.grfc_last_launch_count())
+
+
+def dft_naive_c2c(counts, d_in: int, d_out: int, sign: int, stream: int = 0):
+    """Direct-sum O(P^2) DFT (the drop-in's NaiveDftBackend), same conventions as dft_c2c."""
+    _check(_lib.grfc_dft_naive_c2c(len(counts), _i64(counts), C.c_void_p(d_in), C.c_void_p(d_out), sign,
+                                   C.c_void_p(stream)))
 
 
 def dft_c2c(counts, d_in: int, d_out: int, sign: int, stream: int = 0):
