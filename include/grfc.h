@@ -197,6 +197,13 @@ grfc_status grfc_slab_pass_a(grfc_plan plan, int world, int rank, uint64_t seed,
                              void* stream);
 grfc_status grfc_slab_pass_b(grfc_plan plan, int world, const void* d_recv, void* d_out, void* stream);
 
+/* GridSpec validation (replaces GridSpec::GridSpec's checks, src/grid.cpp:10-30):
+ * dim >= 1, every counts[i] even and >= 2, every lengths[i] finite and > 0
+ * (lengths may be NULL: counts only), prod counts fits int64. GRFC_EINVAL with
+ * the reason in grfc_last_error(); *points = prod counts on success (may be
+ * NULL). Any dim (plans additionally need dim <= 8). Host-only. */
+grfc_status grfc_grid_check(int dim, const int64_t* counts, const double* lengths, int64_t* points);
+
 /* Plan grid: dim, counts[dim], lengths[dim], dtype and device (any output may be NULL). */
 grfc_status grfc_plan_grid(grfc_plan plan, int* dim, int64_t* counts, double* lengths, int* dtype, int* device);
 

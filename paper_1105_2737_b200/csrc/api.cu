@@ -334,6 +334,13 @@ grfc_status grfc_half_noise_from_draws(int dim, const int64_t* counts, int algor
   return GRFC_OK;
 }
 
+grfc_status grfc_grid_check(int dim, const int64_t* counts, const double* lengths, int64_t* points) {
+  if (dim > 0 && !counts) return fail(GRFC_EINVAL, "grfc: null argument");
+  std::string err;
+  if (!check_grid_spec(dim, counts, lengths, points, err)) return fail(GRFC_EINVAL, err);
+  return GRFC_OK;
+}
+
 grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, const double* lengths, int dtype,
                              int algorithm, const grfc_density* density, int device) {
   if (!out || !counts || !lengths) return fail(GRFC_EINVAL, "grfc: null argument");

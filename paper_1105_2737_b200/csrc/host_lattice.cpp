@@ -5,31 +5,25 @@
 
 namespace grfc {
 
-bool validate_grid(int d, const int64_t* n, const double* l, std::string& err) {
-  if (d < 1) {
-    err = "GridSpec: dimension must be >= 1";
-    return false;
-  }
-  if (d > 8) {
-    err = "grfc: dimension > 8 not supported";
-    return false;
-  }
+// GridSpec rules (reference grid.cpp:10-30): d >= 1; every N_i even and >= 2;
+// every l_i finite and > 0 (skipped when l is null); prod N_i fits int64.
+bool check_grid_spec(int d, const int64_t* n, const double* l, int64_t* points, std::string& err) {
+  if (d < 1) return err = "GridSpec: dimension must be >= 1", false;
   int64_t p = 1;
   for (int a = 0; a < d; ++a) {
-    if (n[a] < 2 || n[a] % 2 != 0) {
-      err = "GridSpec: point counts must be even and >= 2";
-      return false;
-    }
-    if (l && (!(l[a] > 0.0) || !std::isfinite(l[a]))) {
-      err = "GridSpec: edge lengths must be positive and finite";
-      return false;
-    }
-    if (p > std::numeric_limits<int64_t>::max() / n[a]) {
-      err = "GridSpec: total point count overflows";
-      return false;
-    }
+    if (n[a] < 2 || (n[a] & 1)) return err = "GridSpec: point counts must be even and >= 2", false;
+    if (l && !(std::isfinite(l[a]) && l[a] > 0.0))
+      return err = "GridSpec: edge lengths must be positive and finite", false;
+    if (p > std::numeric_limits<int64_t>::max() / n[a]) return err = "GridSpec: total point count overflows", false;
     p *= n[a];
   }
+  if (points) *points = p;
+  return true;
+}
+
+bool validate_grid(int d, const int64_t* n, const double* l, std::string& err) {
+  if (!check_grid_spec(d, n, l, nullptr, err)) return false;
+  if (d > 8) return err = "grfc: dimension > 8 not supported", false;
   return true;
 }
 

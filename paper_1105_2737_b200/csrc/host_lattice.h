@@ -11,7 +11,10 @@
 
 namespace grfc {
 
-// GridSpec validation, src/grid.cpp:10-30 (lengths may be null: counts only).
+// GridSpec validation, src/grid.cpp:10-30 (lengths may be null: counts only);
+// any d >= 1. *points = prod N_i when valid (points may be null).
+bool check_grid_spec(int d, const int64_t* counts, const double* lengths, int64_t* points, std::string& err);
+// check_grid_spec plus the device path's d <= 8.
 bool validate_grid(int d, const int64_t* counts, const double* lengths, std::string& err);
 
 // count_draws, src/synth.cpp:211-218 + src/hermitian.cpp:228-236.

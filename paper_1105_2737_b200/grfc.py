@@ -112,6 +112,7 @@ def _load():
         "grfc_generate_injected_host": [P, P, C.c_uint64, P],
         "grfc_dft_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_dft_naive_c2c": [C.c_int, P, P, P, C.c_int, P],
+        "grfc_grid_check": [C.c_int, P, P, P],
         "grfc_dft_naive_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_conjugate_reps": [C.c_int, P, P, P, C.c_uint64, P],
         "grfc_slab_sizes": [P, C.c_int, P, P, P],
@@ -150,7 +151,7 @@ EXPORTED = (
     "grfc_slab_pass_a", "grfc_slab_pass_b", "grfc_estimate_covariance", "grfc_estimate_covariance_host",
     "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
     "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1", "grfc_measure_fp32_peak",
-    "grfc_dft_naive_c2c", "grfc_dft_naive_c2c_host",
+    "grfc_dft_naive_c2c", "grfc_dft_naive_c2c_host", "grfc_grid_check",
 )
 
 
