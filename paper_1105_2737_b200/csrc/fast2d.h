@@ -29,7 +29,6 @@ struct Fast2D {
   int kind = 0;
   // persistent fused kernel geometry (fused_query)
   bool persistent = false;
-  bool warp = false;  // warp-synchronous column tiles + transposed W (fast2d_warp.cuh)
   int occ = 1, sms = 148, strips = 0, rtiles = 0;
   // cluster-scheduled fused kernel (k_fused2d_cl): CTAs per cluster (0 = off),
   // W slots per cluster, resident clusters

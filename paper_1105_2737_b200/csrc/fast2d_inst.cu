@@ -3,7 +3,6 @@
 // -DINST_T=<float|double> -DINST_N=<N1> so the objects build in parallel.
 // Rows are instantiated for M = N1/2 (covers every supported N2 = 2M).
 #include "fast2d_alg1.cuh"
-#include "fast2d_warp.cuh"
 
 namespace grfc {
 template cudaError_t launch_cols<INST_T, INST_N, GRFC_ONE_FFT_OVERWRITE>(const Fast2D&, uint64_t, uint64_t, int64_t,
@@ -24,17 +23,6 @@ GRFC_FUSED(256)
 GRFC_FUSED(512)
 GRFC_FUSED(1024)
 GRFC_FUSED(2048)
-#if INST_N == 256 || INST_N == 512
-#define GRFC_WARP(M)                                                                                             \
-  template cudaError_t launch_fusedw<INST_T, INST_N, M>(const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*,   \
-                                                        int64_t, cudaStream_t);                                    \
-  template cudaError_t fusedw_query<INST_T, INST_N, M>(Fast2D&);
-GRFC_WARP(128)
-GRFC_WARP(256)
-GRFC_WARP(512)
-GRFC_WARP(1024)
-GRFC_WARP(2048)
-#endif
 // Algorithm 1 (three-tile persistent kernel): square grids, M = N1/2.
 template cudaError_t launch_fused_alg1<INST_T, INST_N, INST_N / 2>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,
                                                                   int64_t, cudaStream_t);

@@ -22,11 +22,6 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
 template <typename T, int N1, int M, int ALG>
 cudaError_t fused_query(Fast2D& f);
 template <typename T, int N1, int M>
-cudaError_t launch_fusedw(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
-                          int64_t stride, cudaStream_t s);
-template <typename T, int N1, int M>
-cudaError_t fusedw_query(Fast2D& f);
-template <typename T, int N1, int M>
 cudaError_t launch_cluster(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
                            int64_t stride, cudaStream_t s);
 template <typename T, int N1, int M>
@@ -147,34 +142,13 @@ static cudaError_t dispatch_clquery(Fast2D& f, int cs, int nsl) {
   GRFC_DISPATCH_N1(T, 0, GRFC_CALL_CLQ)
 }
 
-#define GRFC_CALL_WQ(T, N1, M, ALG) fusedw_query<T, N1, M>(f)
-#define GRFC_CALL_W(T, N1, M, ALG) launch_fusedw<T, N1, M>(f, seed, field0, nf, W, out, stride, s)
-#define GRFC_DISPATCH_N1W(T, CALL)                       \
-  switch (f.n1) {                                       \
-    case 256: { GRFC_DISPATCH_M(T, 256, 0, CALL) }      \
-    case 512: { GRFC_DISPATCH_M(T, 512, 0, CALL) }      \
-  }                                                     \
-  return cudaErrorNotSupported;
-
-template <typename T>
-static cudaError_t dispatch_wquery(Fast2D& f) {
-  GRFC_DISPATCH_N1W(T, GRFC_CALL_WQ)
-}
-
-template <typename T>
-static cudaError_t dispatch_w(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
-                              int64_t stride, cudaStream_t s) {
-  GRFC_DISPATCH_N1W(T, GRFC_CALL_W)
-}
-
 template <typename T>
 static cudaError_t run_fast(const Fast2D& f, int alg, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                             int64_t stride, cudaStream_t s) {
   if (f.persistent && f.cluster && alg == GRFC_ONE_FFT_OVERWRITE)
     return dispatch_cluster<T>(f, seed, field0, nf, W, out, stride, s);
   if (f.persistent && alg == GRFC_ONE_FFT_OVERWRITE)
-    return f.warp ? dispatch_w<T>(f, seed, field0, nf, W, out, stride, s)
-                  : dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s);
+    return dispatch_fused<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, out, stride, s);
   cudaError_t e = alg == GRFC_ONE_FFT_OVERWRITE ? dispatch_cols<T, GRFC_ONE_FFT_OVERWRITE>(f, seed, field0, nf, W, s)
                                                 : dispatch_cols<T, GRFC_ONE_FFT_RECURSIVE>(f, seed, field0, nf, W, s);
   if (e != cudaSuccess) return e;
@@ -275,12 +249,6 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   if (alg != GRFC_ONE_FFT_OVERWRITE) f.persistent = false;
   if (!f.persistent) return cudaSuccess;
   f.fail_what = "persistent kernel query";
-  // Warp-synchronous variant for N1 in {256, 512} (GRFC_WARP=0 disables it).
-  // GRFC_WARP=1 selects the warp-synchronous variant (fast2d_warp.cuh) for N1 in {256, 512}.
-  const char* we = std::getenv("GRFC_WARP");
-  f.warp = (f.n1 == 256 || f.n1 == 512) && we && we[0] == '1';
-  if (f.warp)
-    return dtype == GRFC_F64 ? dispatch_wquery<double>(f) : dispatch_wquery<float>(f);
   e = dtype == GRFC_F64 ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
                         : dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f);
   if (e != cudaSuccess) return e;

@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B the free-form variant libraries (build/libgrfc_x*.so) on config c2; GRFC_WARP picks the 2D variant.
+# A/B the free-form variant libraries (build/libgrfc_x*.so) on config c2.
 cd "$(dirname "$0")/.."
 for lib in paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_x*.so; do
   r=$(GRFC_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} 2>&1 | tail -1 |
