@@ -438,15 +438,17 @@ def run_slab(args, cfg):
     dens = grfc.Density.gaussian_cov(d, cfg["density"][1])
     plan = grfc.Plan(counts, (1.0,) * d, dens, grfc.ONE_FFT_OVERWRITE, grfc.F32, device=local)
     buf, block, slab_pts = plan.slab_sizes(world)
-    send = torch.empty(2 * buf, dtype=torch.float32, device="cuda")  # complex64 as float pairs
-    recv = torch.empty_like(send)
     out = torch.empty(slab_pts, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    # the library's own data plane: an NCCL communicator bootstrapped from rank 0's
+    # unique id (broadcast over the torch process group), then per field
+    # grfc_slab_generate = pass A -> grouped ncclSend/ncclRecv -> pass B
+    uid = [grfc.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = grfc.Comm(uid[0], world, rank, local)
 
     def step(field):
-        plan.slab_pass_a(world, rank, 0, field, send.data_ptr(), stream.cuda_stream)
-        dist.all_to_all_single(recv, send)
-        plan.slab_pass_b(world, recv.data_ptr(), out.data_ptr(), stream.cuda_stream)
+        plan.slab_generate(comm, 0, field, out.data_ptr(), stream.cuda_stream)
 
     for i in range(args.warmup):
         step(i)
@@ -486,7 +488,7 @@ def run_slab(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "config": args.config, "counts": list(counts),
-                       "parallelism": f"slab x{world} (NCCL all_to_all_single between pass A and pass B)",
+                       "parallelism": f"slab x{world} (grfc_slab_generate: pass A, NCCL grouped send/recv, pass B)",
                        "path": plan.path, "l2": "output 512 MiB per step > L2"},
             "path_roofline": {"bound": "hbm", "achieved": P * 4 / (ms / 1e3) / 1e9 / world, "peak": peak,
                               "unit": "GB/s per GPU", "frac": P * 4 / (ms / 1e3) / 1e9 / world / peak},
@@ -496,6 +498,7 @@ def run_slab(args, cfg):
             "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "cpu_baseline": None,
         }
         emit(line)
+    del comm
     dist.destroy_process_group()
 
 

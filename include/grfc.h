@@ -197,6 +197,27 @@ grfc_status grfc_slab_pass_a(grfc_plan plan, int world, int rank, uint64_t seed,
                              void* stream);
 grfc_status grfc_slab_pass_b(grfc_plan plan, int world, const void* d_recv, void* d_out, void* stream);
 
+/* NCCL communicator of the slab path (one process per GPU). Bootstrap: rank 0
+ * calls grfc_comm_unique_id, the host framework broadcasts the
+ * GRFC_UNIQUE_ID_BYTES bytes, every rank calls grfc_comm_create with its rank
+ * and CUDA device (ncclGetUniqueId / ncclCommInitRank; NCCL is loaded at run
+ * time, GRFC_ENCCL if it is absent). */
+#define GRFC_UNIQUE_ID_BYTES 128
+typedef struct grfc_comm_s* grfc_comm;
+grfc_status grfc_comm_unique_id(unsigned char* id);
+grfc_status grfc_comm_create(grfc_comm* out, const unsigned char* id, int world, int rank, int device);
+void grfc_comm_destroy(grfc_comm comm);
+grfc_status grfc_comm_info(grfc_comm comm, int* world, int* rank, int* device);
+/* The all-to-all step above over `comm` (grouped ncclSend/ncclRecv; the
+ * rank's own block is a device copy), enqueued on `stream`. */
+grfc_status grfc_slab_exchange(grfc_plan plan, grfc_comm comm, const void* d_send, void* d_recv, void* stream);
+/* One field (seed, field) over all ranks of `comm`: pass A -> exchange ->
+ * pass B; d_out = this rank's planes j0 in [rank N0/world, ...) (slab_points
+ * reals). Scratch is stream-ordered; asynchronous on `stream`. Fields are
+ * bit-identical to grfc_generate's for every world size. */
+grfc_status grfc_slab_generate(grfc_plan plan, grfc_comm comm, uint64_t seed, uint64_t field, void* d_out,
+                               void* stream);
+
 /* GridSpec validation (replaces GridSpec::GridSpec's checks, src/grid.cpp:10-30):
  * dim >= 1, every counts[i] even and >= 2, every lengths[i] finite and > 0
  * (lengths may be NULL: counts only), prod counts fits int64. GRFC_EINVAL with

@@ -133,7 +133,7 @@ constexpr int planes_min_blocks() {
 template <typename T, int N0, int ALG>
 __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T, N0>())
     k_3d_colgen(F3Params p, PhiloxKey key, uint64_t fld, C_t<T>* __restrict__ W, int k1_lo, int k1_cnt,
-                const C_t<T>* __restrict__ tw0, const C_t<T>* __restrict__ tw2) {
+                int a_lo0, int a_n0, int a_lo1, const C_t<T>* __restrict__ tw0, const C_t<T>* __restrict__ tw2) {
   using C = C_t<T>;
   using PL = ColPlan3<N0, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 4 * CB, TT = N0 / E;
@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* sm = reinterpret_cast<C*>(smem_raw);
   const int strips = p.m / (2 * CB);
-  const int a = (int)(blockIdx.x / (unsigned)strips), s = (int)(blockIdx.x % (unsigned)strips);
+  // tile rows a (quad {k1 = a, k1 = -a}): only those with a row in the rank's slab
+  // [k1_lo, k1_lo + k1_cnt), as at most two intervals [a_lo0, +a_n0), [a_lo1, ...)
+  const int ai = (int)(blockIdx.x / (unsigned)strips), s = (int)(blockIdx.x % (unsigned)strips);
+  const int a = ai < a_n0 ? a_lo0 + ai : a_lo1 + (ai - a_n0);
   const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
   const int h = slot / (2 * CB), side = (slot / CB) & 1, c = slot % CB;
   const int k1 = h == 0 ? a : (p.n1 - a) % p.n1;

@@ -2,7 +2,9 @@
 // fast3d_inst.cu).
 #pragma once
 
+#include <algorithm>
 #include <cstdio>
+#include <utility>
 
 #include "fast2d.h"
 #include "fast3d.h"
@@ -49,12 +51,31 @@ cudaError_t launch_3d_colgen(const Fast3D& f, uint64_t seed, uint64_t field, voi
   // set on every launch: the attribute is per device (a process may use several)
   cudaFuncSetAttribute(k_3d_colgen<T, N0, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int strips = (f.n2 / 2) / (2 * CB);
-  const unsigned blocks = (unsigned)((f.n1 / 2 + 1) * strips);
+  // The tile of row a generates k1 = a and k1 = -a (the Hermitian partner its
+  // pre-twiddle needs); a rank launches only the rows a for which either lies in
+  // its slab: a in [lo, hi) (k1 = a) or -a in [lo, hi), i.e. a in [N1-hi+1, N1-lo]
+  // (k1 = N1 - a), both clipped to [0, N1/2] — at most two intervals.
+  const int half = f.n1 / 2, hi = k1_lo + k1_cnt;
+  int l0 = k1_lo, h0 = std::min(hi, half + 1);              // [l0, h0)
+  int l1 = std::max(f.n1 - hi + 1, 1), h1 = std::min(f.n1 - k1_lo, half) + 1;  // [l1, h1)
+  if (h0 <= l0) l0 = h0 = 0;
+  if (h1 <= l1) l1 = h1 = 0;
+  if (h0 > l0 && h1 > l1 && l1 <= h0 && l0 <= h1) {  // overlapping or adjacent: one interval
+    l0 = std::min(l0, l1);
+    h0 = std::max(h0, h1);
+    l1 = h1 = 0;
+  } else if (h0 <= l0 || (h1 > l1 && l1 < l0)) {  // keep the lower interval first
+    std::swap(l0, l1);
+    std::swap(h0, h1);
+  }
+  const int rows = (h0 - l0) + (h1 - l1);
+  if (rows == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)(rows * strips);
   const C* tw0 = (const C*)f.d_tw;
   const C* tw2 = tw0 + f.n0 + f.n1;
   LaunchScope ls("fused3d_colgen", s);
-  k_3d_colgen<T, N0, ALG><<<blocks, colgen3_threads<N0, T>(), smem, s>>>(make_params3(f), philox_key(seed), field,
-                                                                        (C*)W, k1_lo, k1_cnt, tw0, tw2);
+  k_3d_colgen<T, N0, ALG><<<blocks, colgen3_threads<N0, T>(), smem, s>>>(
+      make_params3(f), philox_key(seed), field, (C*)W, k1_lo, k1_cnt, l0, h0 - l0, l1, tw0, tw2);
   return cudaGetLastError();
 }
 

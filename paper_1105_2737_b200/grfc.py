@@ -113,6 +113,11 @@ def _load():
         "grfc_dft_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_dft_naive_c2c": [C.c_int, P, P, P, C.c_int, P],
         "grfc_grid_check": [C.c_int, P, P, P],
+        "grfc_comm_unique_id": [P],
+        "grfc_comm_create": [P, P, C.c_int, C.c_int, C.c_int],
+        "grfc_comm_info": [P, P, P, P],
+        "grfc_slab_exchange": [P, P, P, P, P],
+        "grfc_slab_generate": [P, P, C.c_uint64, C.c_uint64, P, P],
         "grfc_dft_naive_c2c_host": [C.c_int, P, P, P, C.c_int, C.c_int],
         "grfc_conjugate_reps": [C.c_int, P, P, P, C.c_uint64, P],
         "grfc_slab_sizes": [P, C.c_int, P, P, P],
@@ -134,6 +139,8 @@ def _load():
         fn.restype = C.c_int
     lib.grfc_plan_destroy.argtypes = [P]
     lib.grfc_plan_destroy.restype = None
+    lib.grfc_comm_destroy.argtypes = [P]
+    lib.grfc_comm_destroy.restype = None
     lib.grfc_kernel_timing_enable.argtypes = [C.c_int]
     lib.grfc_kernel_timing_enable.restype = None
     return lib
@@ -152,6 +159,8 @@ EXPORTED = (
     "grfc_covariance_partials", "grfc_covariance_merge", "grfc_covariance_accumulate",
     "grfc_covariance_chunk_injected_host", "grfc_plan_grid", "grfc_write_grf1", "grfc_measure_fp32_peak",
     "grfc_dft_naive_c2c", "grfc_dft_naive_c2c_host", "grfc_grid_check",
+    "grfc_comm_unique_id", "grfc_comm_create", "grfc_comm_destroy", "grfc_comm_info", "grfc_slab_exchange",
+    "grfc_slab_generate",
 )
 
 
@@ -289,6 +298,35 @@ def dft_c2c(counts, d_in: int, d_out: int, sign: int, stream: int = 0):
                              C.c_void_p(stream)))
 
 
+UNIQUE_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; broadcast the bytes to every rank)."""
+    buf = (C.c_ubyte * UNIQUE_ID_BYTES)()
+    _check(_lib.grfc_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """NCCL communicator of the slab path (grfc_comm_create: one per rank and GPU)."""
+
+    def __init__(self, unique_id: bytes, world: int, rank: int, device: int = 0):
+        if len(unique_id) != UNIQUE_ID_BYTES:
+            raise ValueError("unique id must be %d bytes" % UNIQUE_ID_BYTES)
+        buf = (C.c_ubyte * UNIQUE_ID_BYTES).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _check(_lib.grfc_comm_create(C.byref(h), buf, world, rank, device))
+        self._h = h
+        self.world, self.rank, self.device = world, rank, device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.grfc_comm_destroy(h)
+            self._h = None
+
+
 class Plan:
     """One (grid, density, algorithm, precision) bound to a device."""
 
@@ -362,6 +400,15 @@ class Plan:
 
     def slab_pass_a(self, world: int, rank: int, seed: int, field: int, d_send: int, stream: int = 0):
         _check(_lib.grfc_slab_pass_a(self._h, world, rank, seed, field, C.c_void_p(d_send), C.c_void_p(stream)))
+
+    def slab_generate(self, comm: "Comm", seed: int, field: int, d_out: int, stream: int = 0):
+        """One field over all ranks of comm (pass A -> NCCL all-to-all -> pass B); d_out = this
+        rank's planes (slab_sizes(world)[2] reals)."""
+        _check(_lib.grfc_slab_generate(self._h, comm._h, seed, field, C.c_void_p(d_out), C.c_void_p(stream)))
+
+    def slab_exchange(self, comm: "Comm", d_send: int, d_recv: int, stream: int = 0):
+        _check(_lib.grfc_slab_exchange(self._h, comm._h, C.c_void_p(d_send), C.c_void_p(d_recv),
+                                       C.c_void_p(stream)))
 
     def slab_pass_b(self, world: int, d_recv: int, d_out: int, stream: int = 0):
         _check(_lib.grfc_slab_pass_b(self._h, world, C.c_void_p(d_recv), C.c_void_p(d_out), C.c_void_p(stream)))
