@@ -203,8 +203,8 @@ static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64
       for (int b = a + 1; b < d - 1; ++b) inner *= p->n[b];
       for (int b = 0; b < a; ++b) outer *= p->n[b];
       cudaError_t e = launch_line_c2c<T>(W, (int)p->n[a], inner, outer, sign, p->F[a], p->tw(a), s);
-      if (e == cudaErrorInvalidValue)
-        return fail(GRFC_EINVAL, "grfc: axis length " + std::to_string(p->n[a]) + " exceeds the on-chip line limit");
+      // longer than one CTA's shared memory: four-step / Bluestein through global memory
+      if (e == cudaErrorInvalidValue) e = long_c2c<T>(W, p->n[a], inner, outer, sign, s);
       GRFC_CUDA(e);
     }
     return GRFC_OK;
@@ -212,17 +212,19 @@ static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64
   grfc_status st;
   if (p->alg == GRFC_TWO_FFT) {
     cudaError_t e = launch_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, p->FM, p->tw(d - 1), s);
-    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: last-axis length exceeds the on-chip line limit");
+    if (e == cudaErrorInvalidValue) e = long_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, s);
     GRFC_CUDA(e);
     if ((st = axes(+1)) != GRFC_OK) return st;
     GRFC_CUDA(launch_scale_half<T>(p->g, p->D, p->s_two, W, nf, s));
     if ((st = axes(-1)) != GRFC_OK) return st;
-    GRFC_CUDA(launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, p->FM, p->tw(d - 1), s));
+    e = launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, p->FM, p->tw(d - 1), s);
+    if (e == cudaErrorInvalidValue) e = long_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, s);
+    GRFC_CUDA(e);
   } else {
     GRFC_CUDA(launch_gen_half<T>(p->g, p->D, p->alg, p->s_one, seed, field0, inj_half, W, nf, s));
     if ((st = axes(+1)) != GRFC_OK) return st;
     cudaError_t e = launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, p->FM, p->tw(d - 1), s);
-    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: last-axis length exceeds the on-chip line limit");
+    if (e == cudaErrorInvalidValue) e = long_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, s);
     GRFC_CUDA(e);
   }
   return GRFC_OK;
@@ -684,7 +686,7 @@ grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, dou
     for (int b = a + 1; b < dim; ++b) inner *= counts[b];
     for (int b = 0; b < a; ++b) outer *= counts[b];
     cudaError_t e = launch_line_c2c<double>(d_out, (int)n, inner, outer, sign > 0 ? +1 : -1, factorize(n), tw, s);
-    if (e == cudaErrorInvalidValue) return fail(GRFC_EINVAL, "grfc: axis length exceeds the on-chip line limit");
+    if (e == cudaErrorInvalidValue) e = long_c2c<double>(d_out, n, inner, outer, sign > 0 ? +1 : -1, s);
     GRFC_CUDA(e);
   }
   if (sign < 0) GRFC_CUDA(launch_scale_all<double>(d_out, P, 1.0 / (double)P, s));

@@ -36,6 +36,18 @@ template <typename T>
 cudaError_t launch_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, uint64_t seed, uint64_t field,
                                 double* out, cudaStream_t s);
 
+// Lines longer than the on-chip kernels hold (long_fft.cu): four-step / Bluestein
+// through global memory; same conventions as launch_line_c2c / c2r_last /
+// r2c_last_noise (twiddle tables cached per length).
+template <typename T>
+cudaError_t long_c2c(void* data, int64_t n, int64_t inner, int64_t outer, int sign, cudaStream_t s);
+template <typename T>
+cudaError_t long_c2r_last(const void* W, void* out, int64_t n, int64_t rows, int64_t rows_per_field,
+                          int64_t out_field_stride, int conj, cudaStream_t s);
+template <typename T>
+cudaError_t long_r2c_last_noise(void* W, int64_t n, int64_t rows, int64_t rows_per_field, uint64_t seed,
+                                uint64_t field0, const double* injected, cudaStream_t s);
+
 // Covariance estimator kernels (stats.cu).
 cudaError_t launch_cov_accumulate(int dtype, const void* fields, uint64_t nf, uint64_t stride, uint64_t P,
                                   uint64_t ref, double* acc, cudaStream_t s);
