@@ -196,15 +196,16 @@ grfc_status grfc_slab_generate(grfc_plan plan, grfc_comm c, uint64_t seed, uint6
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   void* ws = nullptr;  // send | recv, stream-ordered from the device pool
-  cudaError_t e = cudaMallocAsync(&ws, 2 * bytes, s);
+  // world 1: the exchange is the identity, pass B reads pass A's buffer
+  cudaError_t e = cudaMallocAsync(&ws, (c->world > 1 ? 2 : 1) * bytes, s);
   if (e != cudaSuccess) {
     cudaSetDevice(prev);
     return cuda_fail(e, "slab buffers");
   }
   void* send = ws;
-  void* recv = static_cast<char*>(ws) + bytes;
+  void* recv = c->world > 1 ? static_cast<char*>(ws) + bytes : ws;
   st = grfc_slab_pass_a(plan, c->world, c->rank, seed, field, send, stream);
-  if (st == GRFC_OK) st = grfc_slab_exchange(plan, c, send, recv, stream);
+  if (st == GRFC_OK && c->world > 1) st = grfc_slab_exchange(plan, c, send, recv, stream);
   if (st == GRFC_OK) st = grfc_slab_pass_b(plan, c->world, recv, d_out, stream);
   cudaFreeAsync(ws, s);
   cudaSetDevice(prev);
