@@ -202,8 +202,11 @@ static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64
       int64_t inner = p->n[d - 1] / 2 + 1, outer = nf;
       for (int b = a + 1; b < d - 1; ++b) inner *= p->n[b];
       for (int b = 0; b < a; ++b) outer *= p->n[b];
-      cudaError_t e = launch_line_c2c<T>(W, (int)p->n[a], inner, outer, sign, p->F[a], p->tw(a), s);
-      // longer than one CTA's shared memory: four-step / Bluestein through global memory
+      // longer than one CTA's shared memory, or a long prime factor: four-step /
+      // Bluestein through global memory
+      cudaError_t e = needs_long_line(p->n[a], sizeof(C_t<T>))
+                          ? long_c2c<T>(W, p->n[a], inner, outer, sign, s)
+                          : launch_line_c2c<T>(W, (int)p->n[a], inner, outer, sign, p->F[a], p->tw(a), s);
       if (e == cudaErrorInvalidValue) e = long_c2c<T>(W, p->n[a], inner, outer, sign, s);
       GRFC_CUDA(e);
     }
@@ -211,19 +214,25 @@ static grfc_status run_fields(grfc_plan p, uint64_t seed, uint64_t field0, int64
   };
   grfc_status st;
   if (p->alg == GRFC_TWO_FFT) {
-    cudaError_t e = launch_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, p->FM, p->tw(d - 1), s);
+    const bool long_last = needs_long_line(nd / 2, sizeof(C_t<T>));
+    cudaError_t e = long_last ? cudaErrorInvalidValue
+                              : launch_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, p->FM,
+                                                         p->tw(d - 1), s);
     if (e == cudaErrorInvalidValue) e = long_r2c_last_noise<T>(W, nd, rows, rows_pf, seed, field0, inj_points, s);
     GRFC_CUDA(e);
     if ((st = axes(+1)) != GRFC_OK) return st;
     GRFC_CUDA(launch_scale_half<T>(p->g, p->D, p->s_two, W, nf, s));
     if ((st = axes(-1)) != GRFC_OK) return st;
-    e = launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, p->FM, p->tw(d - 1), s);
+    e = long_last ? cudaErrorInvalidValue
+                  : launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, p->FM, p->tw(d - 1), s);
     if (e == cudaErrorInvalidValue) e = long_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 1, s);
     GRFC_CUDA(e);
   } else {
     GRFC_CUDA(launch_gen_half<T>(p->g, p->D, p->alg, p->s_one, seed, field0, inj_half, W, nf, s));
     if ((st = axes(+1)) != GRFC_OK) return st;
-    cudaError_t e = launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, p->FM, p->tw(d - 1), s);
+    cudaError_t e = needs_long_line(nd / 2, sizeof(C_t<T>))
+                        ? cudaErrorInvalidValue
+                        : launch_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, p->FM, p->tw(d - 1), s);
     if (e == cudaErrorInvalidValue) e = long_c2r_last<T>(W, out, nd, rows, rows_pf, stride, 0, s);
     GRFC_CUDA(e);
   }
@@ -685,7 +694,9 @@ grfc_status grfc_dft_c2c(int dim, const int64_t* counts, const double* d_in, dou
     int64_t inner = 1, outer = 1;
     for (int b = a + 1; b < dim; ++b) inner *= counts[b];
     for (int b = 0; b < a; ++b) outer *= counts[b];
-    cudaError_t e = launch_line_c2c<double>(d_out, (int)n, inner, outer, sign > 0 ? +1 : -1, factorize(n), tw, s);
+    cudaError_t e = needs_long_line(n, 16) ? cudaErrorInvalidValue
+                                           : launch_line_c2c<double>(d_out, (int)n, inner, outer, sign > 0 ? +1 : -1,
+                                                                     factorize(n), tw, s);
     if (e == cudaErrorInvalidValue) e = long_c2c<double>(d_out, n, inner, outer, sign > 0 ? +1 : -1, s);
     GRFC_CUDA(e);
   }

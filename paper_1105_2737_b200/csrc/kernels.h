@@ -39,6 +39,9 @@ cudaError_t launch_philox_pairs(const uint64_t* units, int64_t n, uint64_t Uh, u
 // Lines longer than the on-chip kernels hold (long_fft.cu): four-step / Bluestein
 // through global memory; same conventions as launch_line_c2c / c2r_last /
 // r2c_last_noise (twiddle tables cached per length).
+// true when a line of n complex (elem_bytes each) needs long_c2c: too long for one
+// CTA, or a prime factor above the on-chip direct-sum limit
+bool needs_long_line(int64_t n, size_t elem_bytes);
 template <typename T>
 cudaError_t long_c2c(void* data, int64_t n, int64_t inner, int64_t outer, int sign, cudaStream_t s);
 template <typename T>

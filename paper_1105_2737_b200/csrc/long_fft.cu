@@ -33,6 +33,9 @@ Factors factorize(int64_t n);  // api.cu
 namespace {
 
 constexpr size_t kSmemLine = 200 * 1024;  // launch_line_c2c's per-CTA budget
+// longest prime the on-chip kernels sum directly (stockham_pass_any is O(n R) and
+// its fp32 sums lose ~sqrt(R) ulps); longer prime factors go through Bluestein
+constexpr int64_t kMaxDirectRadix = 61;
 
 template <typename T>
 bool line_fits(int64_t n) {
@@ -225,6 +228,13 @@ __global__ void k_r2c_post(const C_t<T>* __restrict__ Zf, C_t<T>* __restrict__ W
   }
 }
 
+int64_t largest_prime_factor(int64_t n) {
+  int64_t best = 1;
+  for (int64_t p = 2; p * p <= n; ++p)
+    while (n % p == 0) best = p, n /= p;
+  return n > 1 ? std::max(best, n) : best;
+}
+
 // largest divisor of n that fits on chip (and is < n); 1 if none >= 2
 template <typename T>
 int64_t chip_divisor(int64_t n) {
@@ -274,22 +284,28 @@ cudaError_t bluestein_via_f64(void* data, int64_t n, int64_t inner, int64_t oute
   return e;
 }
 
+bool needs_long_line(int64_t n, size_t elem_bytes) {
+  return 2 * (size_t)(n + 1) * elem_bytes > kSmemLine || largest_prime_factor(n) > kMaxDirectRadix;
+}
+
 template <typename T>
 cudaError_t long_c2c(void* data, int64_t n, int64_t inner, int64_t outer, int sign, cudaStream_t s) {
   using C = C_t<T>;
   if (n <= 1) return cudaSuccess;
-  if (line_fits<T>(n)) {
+  const int64_t big = largest_prime_factor(n);
+  if (line_fits<T>(n) && big <= kMaxDirectRadix) {
     const C* tw = device_table<T>(n, 0);
     if (!tw) return cudaErrorMemoryAllocation;
     return launch_line_c2c<T>(data, (int)n, inner, outer, sign, factorize(n), tw, s);
   }
-  const int64_t n1 = chip_divisor<T>(n);
+  // split n = n1 n2: the large prime factor on its own (Bluestein below), else the
+  // largest factor that fits on chip
+  const int64_t n1 = big > kMaxDirectRadix ? (big == n ? 1 : big) : chip_divisor<T>(n);
   if (n1 >= 2) {  // four-step
     const int64_t n2 = n / n1;
     const C* tw = device_table<T>(n, 0);
-    const C* tw1 = device_table<T>(n1, 0);
-    if (!tw || !tw1) return cudaErrorMemoryAllocation;
-    cudaError_t e = launch_line_c2c<T>(data, (int)n1, inner * n2, outer, sign, factorize(n1), tw1, s);
+    if (!tw) return cudaErrorMemoryAllocation;
+    cudaError_t e = long_c2c<T>(data, n1, inner * n2, outer, sign, s);
     if (e != cudaSuccess) return e;
     C* scratch = nullptr;
     const size_t bytes = (size_t)(outer * n * inner) * sizeof(C);

@@ -34,6 +34,12 @@ def test_header_symbols_exported():
         assert re.search(rf"\bT {s}\b", out), s
 
 
+def test_no_unresolved_internal_symbols():
+    # a shared library links with undefined symbols; catch a missing definition here
+    out = subprocess.run(["nm", "-C", "-u", grfc.LIB_PATH], capture_output=True, text=True).stdout
+    assert not [ln for ln in out.splitlines() if "grfc::" in ln or " grfc_" in ln], out
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", grfc.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
