@@ -68,6 +68,10 @@ inline void ring_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, 
   *S = s;
   *conc = c;
 }
+// Workspace of the persistent kernel, with occupancy `occ` (may differ per instantiation).
+inline void fused_geometry_occ(const Fast2D& f, int occ, int64_t nf, uint32_t* L, uint32_t* S, uint32_t* conc) {
+  ring_geometry(f.sms, occ, f.strips, f.rtiles, nf, L, S, conc);
+}
 inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S, uint32_t* conc) {
   ring_geometry(f.sms, f.occ, f.strips, f.rtiles, nf, L, S, conc);
 }

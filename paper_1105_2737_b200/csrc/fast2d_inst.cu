@@ -13,7 +13,7 @@ template cudaError_t launch_rows<INST_T, INST_N / 2>(const Fast2D&, int64_t, con
                                                     cudaStream_t);
 #define GRFC_FUSED(M)                                                                                    \
   template cudaError_t launch_fused<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(                                \
-      const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*, int64_t, cudaStream_t);                        \
+      const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*, int64_t, cudaStream_t, const void*);           \
   template cudaError_t fused_query<INST_T, INST_N, M, GRFC_ONE_FFT_OVERWRITE>(Fast2D&);                         \
   template cudaError_t launch_cluster<INST_T, INST_N, M>(const Fast2D&, uint64_t, uint64_t, int64_t, void*, void*,   \
                                                          int64_t, cudaStream_t);                                    \
@@ -23,6 +23,17 @@ GRFC_FUSED(256)
 GRFC_FUSED(512)
 GRFC_FUSED(1024)
 GRFC_FUSED(2048)
+// fp64: the fused kernel over a preloaded X (kPreX, small batches: c1)
+#if INST_T_IS_DOUBLE
+#define GRFC_FUSED_PRE(M)                                                                                      \
+  template cudaError_t launch_fused<double, INST_N, M, kPreX>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,  \
+                                                              void*, int64_t, cudaStream_t, const void*);
+GRFC_FUSED_PRE(128)
+GRFC_FUSED_PRE(256)
+GRFC_FUSED_PRE(512)
+GRFC_FUSED_PRE(1024)
+GRFC_FUSED_PRE(2048)
+#endif
 // Algorithm 1 (three-tile persistent kernel): square grids, M = N1/2.
 template cudaError_t launch_fused_alg1<INST_T, INST_N, INST_N / 2>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,
                                                                   int64_t, cudaStream_t);

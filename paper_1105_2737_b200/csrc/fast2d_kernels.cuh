@@ -35,6 +35,13 @@
 
 namespace grfc {
 
+// Pseudo-algorithm of the fused 2D kernels: the column tiles read X(K) =
+// conj(w) sqrt(g) scale from a buffer filled beforehand by k_gen_half (one cell
+// per thread over the whole GPU) instead of generating it. For fp64 batches too
+// small to fill the GPU with column tiles (c1: one field = 64 tiles), whose
+// IEEE-fp64 generation is FP64-pipe-bound on the SMs that hold column tiles.
+constexpr int kPreX = 8;
+
 // ---------------------------------------------------------------- radix plans
 template <int... Rs>
 struct Radices {};
@@ -104,7 +111,19 @@ GRFC_PLAN(ColPlan, 256, double, 16, 8, 16, 16)
 #ifndef GRFC_COL512D_X
 #define GRFC_COL512D_X 2
 #endif
+// GRFC_COL512D_E: elements per thread of the fp64 512-point column (16: radix 16,16,2;
+// 8: 8,8,8; 4: 4,4,4,4,2) — fewer elements = more threads per column, shorter
+// per-thread generation chains (c1 is one field: latency-bound)
+#ifndef GRFC_COL512D_E
+#define GRFC_COL512D_E 16
+#endif
+#if GRFC_COL512D_E == 8
+GRFC_PLAN(ColPlan, 512, double, 8, GRFC_COL512D_X, 8, 8, 8)
+#elif GRFC_COL512D_E == 4
+GRFC_PLAN(ColPlan, 512, double, 4, GRFC_COL512D_X, 4, 4, 4, 4, 2)
+#else
 GRFC_PLAN(ColPlan, 512, double, 16, GRFC_COL512D_X, 16, 16, 2)
+#endif
 GRFC_PLAN(ColPlan, 1024, double, 16, 4, 16, 16, 4)
 GRFC_PLAN(ColPlan, 2048, double, 16, 2, 16, 16, 8)
 GRFC_PLAN(ColPlan, 4096, double, 16, 1, 16, 16, 16)
@@ -437,6 +456,8 @@ struct F2Params {
   float f_wstep1, f_wstep2, f_sqrt_c, f_ell2, f_nhalf_alpha, f_gauss_k, f_scale;
   float f_lg2K;  // log2(sqrt_c * scale / sqrt 2) for the folded Matern multiplier
   const float* sg;  // Fast2D::d_sg (fp32 Algorithm 2) or nullptr
+  const void* xpre;  // kPreX: X(K) of every half-lattice cell, [field][n1][hd] (k_gen_half)
+  uint64_t xfield0;  // kPreX: field index of xpre's first field
   int family;
   DensityDesc D;
   GridDesc g;
@@ -563,6 +584,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 #define GRFC_GEN_UNROLL 4
 #endif
 constexpr int kGenUnroll = GRFC_GEN_UNROLL;
+// generic generation loop (fp64 and the packed column): independent cells in flight
+#ifndef GRFC_GEN64_UNROLL
+#define GRFC_GEN64_UNROLL 1
+#endif
+constexpr int kGen64Unroll = GRFC_GEN64_UNROLL;
 
 // Group-per-column column tiles (see col_tile): fp32 plans whose column team is
 // several whole warps (N1/E > 32, c3: 256 threads per 4096-point column): each
@@ -645,7 +671,19 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // GRFC_EARLY_REL: release the previous tile before generation (its consumers
   // wait on it; the fence stalls warp 0 only while the others generate)
   if (GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
-  if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && p.sg) {
+  if constexpr (ALG == kPreX) {
+    const C* __restrict__ xs = reinterpret_cast<const C*>(p.xpre) + (uint64_t)(fld - p.xfield0) * N1 * p.hd;
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+      const int k1 = j + t * TT;
+      C x = xs[(int64_t)k1 * p.hd + col];
+      if (packed) {  // column 0 + i * column M
+        const C y = xs[(int64_t)k1 * p.hd + p.m];
+        x = mk<C>(x.x - y.y, x.y + y.x);
+      }
+      gslot(k1) = x;
+    }
+  } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && p.sg) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one Philox
     // call; sqrt(g) scale / sqrt 2 from the plan's per-cell table (L2-resident)
     const float* __restrict__ sgc = p.sg + col;
@@ -698,7 +736,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       gslot(k1 + N1 / 2) = mk<C>((T)a1 * m1, -(T)b1 * m1);
     }
   } else {
-#pragma unroll 1
+#pragma unroll(kGen64Unroll)
     for (int t = 0; t < E; ++t) {
       const int k1 = j + t * TT;
       C x = gen_cell<T, ALG>(p, k1, col, key, fld);
@@ -1187,6 +1225,21 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   }
 }
 
+// X(K) of every half-lattice cell of fields [field0, field0 + nf), one cell per
+// thread over the whole GPU: the same gen_cell the column tiles run, so kPreX
+// fields are bit-identical to generated ones (batch composition never changes
+// a field). Layout [field][k1][hd].
+template <typename T>
+__global__ void __launch_bounds__(256) k_gen_x2d(F2Params p, PhiloxKey key, uint64_t field0, int64_t nf,
+                                                 C_t<T>* __restrict__ X) {
+  const int64_t per = (int64_t)p.n1 * p.hd, total = per * nf;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = e / per, h = e - f * per;
+    const int k1 = (int)(h / p.hd), k2 = (int)(h - (int64_t)k1 * p.hd);
+    X[e] = gen_cell<T, GRFC_ONE_FFT_OVERWRITE>(p, k1, k2, key, field0 + (uint64_t)f);
+  }
+}
+
 // ---------------------------------------------------------------- cluster-scheduled fused kernel
 // One launch per batch, persistent, launched as thread-block clusters of CS
 // CTAs. Cluster c owns fields c, c + nclusters, ...; CTA rank r of the cluster
@@ -1393,13 +1446,30 @@ cudaError_t fused_query(Fast2D& f) {
 
 template <typename T, int N1, int M, int ALG>
 cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
-                         int64_t stride, cudaStream_t s) {
+                         int64_t stride, cudaStream_t s, const void* xpre) {
   using C = C_t<T>;
   constexpr int NT = fused_threads<N1, M, T>();
   constexpr size_t smem = fused_smem<N1, M, T>();
+  F2Params prm = make_params(f);
+  Fast2D geo = f;  // geometry of this instantiation
+  if constexpr (ALG == kPreX) {
+    cudaError_t e = cudaFuncSetAttribute(k_fused2d<T, N1, M, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<T, N1, M, ALG>, NT, smem);
+    if (e != cudaSuccess) return e;
+    geo.occ = occ < 1 ? 1 : occ;
+    prm.xpre = xpre;
+    prm.xfield0 = field0;
+    const int64_t cells = (int64_t)N1 * (M + 1) * nf;
+    LaunchScope ls("gen_x2d", s);
+    k_gen_x2d<T><<<(unsigned)std::min<int64_t>((cells + 255) / 256, (int64_t)f.sms * 16), 256, 0, s>>>(
+        prm, philox_key(seed), field0, nf, (C*)const_cast<void*>(xpre));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   F2Sched q{};
   uint32_t conc = 0;
-  fused_geometry(f, nf, &q.L, &q.S, &conc);
+  fused_geometry(geo, nf, &q.L, &q.S, &conc);
   q.F = (uint32_t)nf;
   q.strips = (uint32_t)f.strips;
   q.rtiles = (uint32_t)f.rtiles;
@@ -1424,8 +1494,7 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   q.stats = dstats;
   {
     LaunchScope ls("fused2d_persistent", s);
-    k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(make_params(f), q, philox_key(seed), field0, ring, (T*)out, stride,
-                                                    tw1, tw2);
+    k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out, stride, tw1, tw2);
   }
   e = cudaGetLastError();
   if (dstats) {

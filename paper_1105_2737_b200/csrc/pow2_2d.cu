@@ -8,6 +8,7 @@
 
 #include "fast2d.h"
 #include "grfc_internal.cuh"
+#include "kernels.h"
 
 namespace grfc {
 
@@ -18,7 +19,8 @@ template <typename T, int M>
 cudaError_t launch_rows(const Fast2D& f, int64_t nf, const void* W, void* out, int64_t stride, cudaStream_t s);
 template <typename T, int N1, int M, int ALG>
 cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* ws, void* out,
-                         int64_t stride, cudaStream_t s);
+                         int64_t stride, cudaStream_t s, const void* xpre);
+constexpr int kPreX = 8;  // fast2d_kernels.cuh
 template <typename T, int N1, int M, int ALG>
 cudaError_t fused_query(Fast2D& f);
 template <typename T, int N1, int M>
@@ -101,7 +103,8 @@ static cudaError_t dispatch_rows(const Fast2D& f, int64_t nf, const void* W, voi
   }                                                        \
   return cudaErrorNotSupported;
 
-#define GRFC_CALL_FUSED(T, N1, M, ALG) launch_fused<T, N1, M, ALG>(f, seed, field0, nf, W, out, stride, s)
+#define GRFC_CALL_FUSED(T, N1, M, ALG) launch_fused<T, N1, M, ALG>(f, seed, field0, nf, W, out, stride, s, nullptr)
+#define GRFC_CALL_FUSED_PRE(T, N1, M, ALG) launch_fused<T, N1, M, ALG>(f, seed, field0, nf, W, out, stride, s, xpre)
 #define GRFC_CALL_QUERY(T, N1, M, ALG) fused_query<T, N1, M, ALG>(f)
 #define GRFC_CALL_ALG1(T, N1, M, ALG) launch_fused_alg1<T, N1, M>(f, seed, field0, nf, out, stride, s)
 
@@ -123,6 +126,11 @@ template <typename T, int ALG>
 static cudaError_t dispatch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W, void* out,
                                   int64_t stride, cudaStream_t s) {
   GRFC_DISPATCH_N1(T, ALG, GRFC_CALL_FUSED)
+}
+
+static cudaError_t dispatch_fused_pre(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* W,
+                                      void* out, int64_t stride, cudaStream_t s, const void* xpre) {
+  GRFC_DISPATCH_N1(double, kPreX, GRFC_CALL_FUSED_PRE)
 }
 
 template <typename T, int ALG>
@@ -306,6 +314,20 @@ cudaError_t fast2d_generate(Fast2D& f, int alg, uint64_t seed, uint64_t field0, 
   if (alg == GRFC_TWO_FFT)  // Algorithm 1: always the persistent three-tile kernel
     return f.dtype == GRFC_F64 ? dispatch_alg1<double>(f, seed, field0, nf, out, stride, s)
                                : dispatch_alg1<float>(f, seed, field0, nf, out, stride, s);
+  if (f.persistent && f.dtype == GRFC_F64 && !f.cluster && nf * f.strips < f.sms) {
+    // a batch whose column tiles cannot fill the GPU (c1: one 512^2 field = 64
+    // tiles): X(K) for every cell first, one cell per thread over all SMs
+    // (k_gen_x2d), then the fused kernel with column tiles that load it (kPreX)
+    const size_t xbytes = (size_t)nf * f.n1 * (f.n2 / 2 + 1) * 16;
+    void* xpre = nullptr;
+    cudaError_t e = cudaMallocAsync(&xpre, xbytes, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync(&ws, fast2d_workspace_bytes(f, nf), s);
+    if (e == cudaSuccess) e = dispatch_fused_pre(f, seed, field0, nf, ws, out, stride, s, xpre);
+    if (ws) cudaFreeAsync(ws, s);
+    cudaFreeAsync(xpre, s);
+    return e;
+  }
   if (f.persistent) {
     cudaError_t e = cudaMallocAsync(&ws, fast2d_workspace_bytes(f, nf), s);
     if (e != cudaSuccess) return e;
