@@ -33,6 +33,8 @@ struct Fast2D {
   // cluster-scheduled fused kernel (k_fused2d_cl): CTAs per cluster (0 = off),
   // W slots per cluster, resident clusters
   int cluster = 0, cslots = 1, nclusters = 0;
+  // scheduler groups of the persistent kernel (group_geometry; read at plan setup)
+  int group = 0, group_L = 1, group_S = 2;
   // two-stream pipeline: column kernels on sa, row kernels on sb, a ring of
   // kRing chunk slots ordered by events (no in-kernel waiting).
   static constexpr int kRing = 3;
@@ -76,6 +78,36 @@ inline void fused_geometry(const Fast2D& f, int64_t nf, uint32_t* L, uint32_t* S
   ring_geometry(f.sms, f.occ, f.strips, f.rtiles, nf, L, S, conc);
 }
 inline size_t fused_ctr_bytes(uint32_t S) { return ((1 + 2 * (size_t)S) * 4 + 255) / 256 * 256; }
+
+// Scheduler groups of the persistent 2D kernel (GRFC_GROUP = CTAs per group,
+// GRFC_GROUP_L / _S = lookahead and ring slots per group): each group is an
+// independent queue over every groups-th field with its own W ring, so the
+// rings' total (groups x S x P*s) can stay L2-resident while each queue keeps
+// its tile-level load balance. groups = 1: the single whole-grid queue.
+struct GroupGeom {
+  uint32_t groups = 1, gsize = 0, L = 0, S = 0;
+};
+inline GroupGeom group_geometry(const Fast2D& f, int64_t nf) {
+  GroupGeom g;
+  const int gs = f.group;
+  const int conc = f.sms * f.occ;
+  if (gs <= 0 || gs >= conc) return g;
+  const uint32_t groups = (uint32_t)(conc / gs);
+  if (groups < 2 || (int64_t)groups > nf) return g;
+  const uint32_t fmin = (uint32_t)(nf / groups);  // smallest group's field count
+  uint32_t L = (uint32_t)f.group_L, S = (uint32_t)f.group_S;
+  L = L < 1 ? 1 : L;
+  S = S < L + 1 ? L + 1 : S;
+  if (L > fmin) L = fmin;
+  if (L < 1) return g;
+  if (S > fmin) S = fmin;
+  if (S < 1) S = 1;
+  g.groups = groups;
+  g.gsize = (uint32_t)gs;
+  g.L = L;
+  g.S = S;
+  return g;
+}
 // Device workspace one persistent launch over nf fields needs.
 size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf);
 

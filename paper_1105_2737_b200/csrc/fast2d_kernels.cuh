@@ -562,6 +562,12 @@ __device__ __forceinline__ C epilogue_z(C X, C P, bool packed, bool mid, C w) {
 #ifndef GRFC_EARLY_REL
 #define GRFC_EARLY_REL 1
 #endif
+// Experiment only (never set in a product build): GRFC_EXP_NOW=1 drops the W
+// stores of column tiles and the W loads of row tiles (fields are garbage) to
+// measure the fused kernel's time without its intermediate memory traffic.
+#ifndef GRFC_EXP_NOW
+#define GRFC_EXP_NOW 0
+#endif
 // ---------------------------------------------------------------- tiles
 // Release-increment of a completion counter: orders this thread's (and, after
 // a CTA barrier, the CTA's) prior writes before the increment. Emits
@@ -603,13 +609,37 @@ constexpr bool col_warp_mode() {
   return GRFC_COLGROUP && sizeof(T) == 4 && N1 / ColPlan<N1, T>::E > 32 && (N1 / ColPlan<N1, T>::E) % 32 == 0 &&
          2 * ColPlan<N1, T>::X <= 15 && 2 * ColPlan<N1, T>::X * (N1 / ColPlan<N1, T>::E) == col_threads<N1, T>();
 }
+// strip-blocked W (wpos) for the long-column plans of the persistent kernels
+#ifndef GRFC_WPERM
+#define GRFC_WPERM 1
+#endif
+template <int N1, typename T>
+constexpr int w_perm_cb() {
+  return (GRFC_WPERM && col_warp_mode<N1, T>()) ? ColPlan<N1, T>::X : 0;
+}
 // per-column region: N1 padded rows + 4 elements (so the regions start 8 banks apart)
 constexpr int wcol_pitch(int n1) { return n1 + n1 / 16 + 4; }
 
-template <typename T, int N1, int MC>
+template <typename T, int N1, int MC, bool PERM = false>
 __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                              const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
                                              int col, bool packed, bool mid);
+
+// Strip-blocked W columns (PERM, the persistent kernels' long-column plans): the
+// column tile of strip s writes its 2CB columns {s CB + c} and {M - s CB - c}
+// (M/2 for s = 0, c = 0) as ONE contiguous run at s 2CB + slot of each W row,
+// so every W store covers whole 32-byte sectors (natural order leaves 2CB/2-
+// column runs: 16 B for c3's CB = 2). wpos maps a natural column k to its
+// position; the row tiles load through it (cb = 0: natural order).
+__device__ __forceinline__ int wpos(int k, int M, int cb) {
+  if (cb == 0) return k;
+  if (2 * k < M) return (k / cb) * 2 * cb + k % cb;
+  if (2 * k == M) return cb;
+  const int m = M - k;
+  return (m / cb) * 2 * cb + cb + m % cb;
+}
+template <int N1, typename T>
+constexpr int w_perm_cb();  // below (needs col_warp_mode)
 
 // Fills the per-CTA radix-16 twiddle table (fp32; see stage_compute) and returns
 // it (nullptr for fp64). Ends with a CTA barrier.
@@ -637,7 +667,7 @@ struct NoHook {
 // scheduler checks the next tile's dependency there, off the critical path.
 // `pre` runs on every thread after the column FFT and before the W stores (the
 // cluster scheduler waits there for the W slot to be free).
-template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook>
+template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook, bool PERM = false>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
@@ -790,13 +820,13 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       __syncthreads();
     }
   }
-  col_epilogue<T, N1, MC>(p, s, Wf, tw2, sm, v, slot, j, col, packed, mid);
+  col_epilogue<T, N1, MC, PERM>(p, s, Wf, tw2, sm, v, slot, j, col, packed, mid);
 }
 
 // Z epilogue + W stores of a column tile, lanes across the strip's slots
 // (slot = tid % SLOTS, team position j = tid / SLOTS). In WCOL mode the FFT
 // results are re-read here from the per-warp regions in that mapping.
-template <typename T, int N1, int MC>
+template <typename T, int N1, int MC, bool PERM>
 __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                              const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
                                              int col, bool packed, bool mid) {
@@ -819,7 +849,7 @@ __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* _
   // one 64-bit pointer per thread; with a compile-time M (persistent kernel) every
   // store is that pointer plus an immediate
   const int64_t mstride = MC > 0 ? (int64_t)MC : (int64_t)p.m;
-  C* __restrict__ wp = Wf + (int64_t)j * mstride + col;
+  C* __restrict__ wp = Wf + (int64_t)j * mstride + (PERM ? s * SLOTS + slot : col);
   // Only the warps of strip 0 hold the packed (0, M) and middle (M/2) columns:
   // the others take a branch-free path (warp-uniform test).
   if (!__any_sync(0xffffffffu, special)) {
@@ -831,7 +861,12 @@ __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* _
         C P;
         P.x = __shfl_xor_sync(0xffffffffu, v[e].x, CB);
         P.y = __shfl_xor_sync(0xffffffffu, v[e].y, CB);
-        __stcg(wp + (b * TT + i * (N1 / RL)) * mstride, epilogue_z<T>(v[e], P, false, false, w));
+        const C z = epilogue_z<T>(v[e], P, false, false, w);
+        if (GRFC_EXP_NOW) {
+          if (z.x == (T)1.2345) __stcg(wp, z);  // keep the arithmetic live
+        } else {
+          __stcg(wp + (b * TT + i * (N1 / RL)) * mstride, z);
+        }
       }
     return;
   }
@@ -871,7 +906,7 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 
 // Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
 // real field rows out. Block = RPT * (M/E) threads.
-template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook>
+template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook, int WPERM = 0>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
                                          const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
                                          uint32_t* sig = nullptr, Hook hook = Hook{}, const C_t<T>* t16 = nullptr) {
@@ -888,7 +923,9 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
 #pragma unroll
   for (int b = 0; b < E / R0; ++b)
 #pragma unroll
-    for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcg(&Wr[j + b * TT + i * (M / R0)]);
+    for (int i = 0; i < R0; ++i)
+      v[b * R0 + i] = GRFC_EXP_NOW ? mk<C>((decltype(C{}.x))(j + b + i), (decltype(C{}.x))row)
+                                   : __ldcg(&Wr[wpos(j + b * TT + i * (M / R0), M, WPERM)]);
   // Release of the CTA's previous tile; its fence overlaps the W loads' latency.
   if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
   if (threadIdx.x == 0) hook();
@@ -952,6 +989,12 @@ struct F2Sched {
   unsigned long long* stats;
   // f / S = umulhi(f, s_magic) when s_magic != 0 (host-checked: F * S < 2^32)
   uint32_t s_magic;
+  // Scheduler groups (GRFC_GROUP): `groups` independent queues of `gsize` CTAs
+  // each; group g runs fields g, g + groups, ... with its own ticket, counters
+  // (ctr_stride words apart) and ring (ring_stride elements apart). F, L, S are
+  // per group; F_total is the batch. groups == 1: one queue over the grid.
+  uint32_t groups, gsize, ctr_stride, F_total;
+  uint64_t ring_stride;
 };
 
 // Ring-slot division of the tile decoder (thread 0, once per tile).
@@ -1036,6 +1079,18 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   // Thread 0 signals tile i's completion after that barrier; only if i+1's
   // dependency was not yet met does it spin and add a second barrier.
   const uint64_t slot_elems = (uint64_t)N1 * M;
+  // scheduler group of this CTA: its own queue over fields gid, gid + groups, ...
+  uint32_t fstep = 1, foff = 0;
+  if (q.groups > 1) {
+    const uint32_t gid = blockIdx.x / q.gsize;
+    q.ticket += (size_t)gid * q.ctr_stride;
+    q.col_done += (size_t)gid * q.ctr_stride;
+    q.row_done += (size_t)gid * q.ctr_stride;
+    ring += gid * q.ring_stride;
+    q.F = (q.F_total - gid + q.groups - 1) / q.groups;
+    fstep = q.groups;
+    foff = gid;
+  }
   // tiles per field are compile-time (strips = M / 2CB, row tiles = N1 / RPT): the
   // decoder's divisions by them are shifts; the ring-slot division is a multiply-high
   constexpr uint32_t STRIPS = M / (2 * ColPlan<N1, T>::X), RT = N1 / RPT, G = STRIPS + RT;
@@ -1185,13 +1240,14 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     };
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
-      col_tile<T, N1, ALG, M>(p, key, field0 + m.f, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
-                              GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr,
-                              hook, t16);
+      col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0)>(
+          p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
+          GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr, hook, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
-                                                     smem_raw, done_ctr, hook, t16);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>(), decltype(hook), w_perm_cb<N1, T>()>(
+          Wf, (int)m.idx * RPT, N1, out + (int64_t)(foff + (uint64_t)m.f * fstep) * out_stride, tw2, smem_raw,
+          done_ctr, hook, t16);
       done_ctr = &q.row_done[m.slot];
     }
     // every tile has internal barriers, so all threads have read s_msg
@@ -1314,7 +1370,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), cl_min_blocks<N1, M
       // (the arrive after its rows); the first column tile waits for that just
       // before its W stores, so the barrier's latency hides behind its FFT.
       const ClusterWaitPre pre{NSL == 1 && first && it > 0};
-      col_tile<T, N1, GRFC_ONE_FFT_OVERWRITE, M, NoHook, ClusterWaitPre>(
+      col_tile<T, N1, GRFC_ONE_FFT_OVERWRITE, M, NoHook, ClusterWaitPre, (w_perm_cb<N1, T>() > 0)>(
           p, key, field0 + f, (int)sidx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, nullptr, 0, nullptr,
           NoHook{}, t16, pre);
       first = false;
@@ -1324,7 +1380,8 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), cl_min_blocks<N1, M
     cluster_arrive();
     cluster_wait();
     for (uint32_t r = rank; r < RT; r += cs) {
-      row_tile<T, M, RPT, NT>(Wf, (int)r * RPT, N1, out + (int64_t)f * out_stride, tw2, smem_raw, nullptr, NoHook{},
+      row_tile<T, M, RPT, NT, NoHook, w_perm_cb<N1, T>()>(Wf, (int)r * RPT, N1, out + (int64_t)f * out_stride, tw2,
+                                                           smem_raw, nullptr, NoHook{},
                               t16);
       __syncthreads();
     }
@@ -1469,22 +1526,34 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   }
   F2Sched q{};
   uint32_t conc = 0;
-  fused_geometry(geo, nf, &q.L, &q.S, &conc);
-  q.F = (uint32_t)nf;
+  const GroupGeom gg = group_geometry(geo, nf);
+  if (gg.groups > 1) {
+    q.L = gg.L;
+    q.S = gg.S;
+    conc = gg.groups * gg.gsize;
+  } else {
+    fused_geometry(geo, nf, &q.L, &q.S, &conc);
+  }
+  q.F = gg.groups > 1 ? (uint32_t)((nf + gg.groups - 1) / gg.groups) : (uint32_t)nf;  // largest group's
+  q.F_total = (uint32_t)nf;
+  q.groups = gg.groups;
+  q.gsize = gg.gsize;
   q.strips = (uint32_t)f.strips;
   q.rtiles = (uint32_t)f.rtiles;
   q.s_magic = slot_magic(q.F, q.S);
-  uint32_t* ctr = (uint32_t*)ws;  // [ticket][col_done S][row_done S] | ring
+  q.ctr_stride = (uint32_t)(fused_ctr_bytes(q.S) / sizeof(uint32_t));
+  q.ring_stride = (uint64_t)q.S * N1 * M;
+  uint32_t* ctr = (uint32_t*)ws;  // per group: [ticket][col_done S][row_done S] (padded) | rings
   q.ticket = ctr;
   q.col_done = ctr + 1;
   q.row_done = ctr + 1 + q.S;
-  C* ring = (C*)((char*)ws + fused_ctr_bytes(q.S));
-  cudaError_t e = cudaMemsetAsync(ctr, 0, (1 + 2 * q.S) * sizeof(uint32_t), s);
+  C* ring = (C*)((char*)ws + fused_ctr_bytes(q.S) * gg.groups);
+  cudaError_t e = cudaMemsetAsync(ctr, 0, fused_ctr_bytes(q.S) * gg.groups, s);
   if (e != cudaSuccess) return e;
   const C* tw1 = (const C*)f.d_tw;
   const C* tw2 = tw1 + f.n1;
   const uint32_t total = q.F * (q.strips + q.rtiles);
-  const uint32_t grid = total < conc ? total : conc;
+  const uint32_t grid = gg.groups > 1 ? conc : (total < conc ? total : conc);
   const char* st = std::getenv("GRFC_TILE_STATS");
   unsigned long long* dstats = nullptr;
   if (st && st[0] == '1') {

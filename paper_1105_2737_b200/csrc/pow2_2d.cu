@@ -260,6 +260,11 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   e = dtype == GRFC_F64 ? dispatch_query<double, GRFC_ONE_FFT_OVERWRITE>(f)
                         : dispatch_query<float, GRFC_ONE_FFT_OVERWRITE>(f);
   if (e != cudaSuccess) return e;
+  // Scheduler groups (group_geometry): GRFC_GROUP = CTAs per group (0: one queue),
+  // GRFC_GROUP_L / GRFC_GROUP_S = lookahead / ring slots per group.
+  if (const char* ge = std::getenv("GRFC_GROUP")) f.group = std::atoi(ge);
+  if (const char* ge = std::getenv("GRFC_GROUP_L")) f.group_L = std::max(1, std::atoi(ge));
+  if (const char* ge = std::getenv("GRFC_GROUP_S")) f.group_S = std::max(1, std::atoi(ge));
   // Cluster-scheduled variant (k_fused2d_cl): GRFC_CLUSTER = CTAs per cluster,
   // GRFC_CSLOTS = W slots per cluster (1 or 2).
   const char* ce = std::getenv("GRFC_CLUSTER");
@@ -277,6 +282,8 @@ size_t fast2d_workspace_bytes(const Fast2D& f, int64_t nf) {
   const size_t slot = (size_t)f.n1 * (size_t)(f.n2 / 2) * (f.dtype == GRFC_F64 ? 16 : 8);
   if (!f.persistent) return slot * (size_t)nf;
   if (f.cluster) return slot * (size_t)f.cslots * (size_t)std::min<int64_t>(f.nclusters, nf);
+  const GroupGeom gg = group_geometry(f, nf);
+  if (gg.groups > 1) return (fused_ctr_bytes(gg.S) + slot * gg.S) * gg.groups;
   uint32_t L, S, c;
   fused_geometry(f, nf, &L, &S, &c);
   return fused_ctr_bytes(S) + slot * S;
