@@ -451,10 +451,15 @@ grfc_status grfc_plan_create(grfc_plan* out, int dim, const int64_t* counts, con
   const bool allow_fast = !(nofast && nofast[0] == '1');
   if (allow_fast && fast2d_supported(dim, counts, dtype, algorithm, density->family)) {
     cudaError_t e = fast2d_init(p->fast2d, p->g, p->D, dtype, algorithm, p->s_one, p->s_two);
-    if (e != cudaSuccess)
+    if (e == cudaErrorNotSupported) {  // no fused kernel for this shape: the generic path
+      fast2d_free(p->fast2d);
+      p->fast2d = Fast2D{};
+    } else if (e != cudaSuccess) {
       return fail(GRFC_ECUDA, std::string("CUDA: fast2d_init (") + p->fast2d.fail_what + "): " + cudaGetErrorString(e));
-    p->fast = true;
-    p->path = fast2d_name(p->fast2d);
+    } else {
+      p->fast = true;
+      p->path = fast2d_name(p->fast2d);
+    }
   }
   if (allow_fast && fast3d_supported(dim, counts, algorithm)) {
     cudaError_t e = fast3d_init(p->fast3d, p->g, p->D, dtype, algorithm, p->s_one);

@@ -372,9 +372,34 @@ inline void alg1_geometry(int sms, int occ, int strips, int rtiles, int64_t nf, 
   *conc = c;
 }
 
+// (N1, M) pairs the three-tile kernel supports: R1 tiles pair rows j1 and
+// j1 + N1/2, so a tile must hold an even number (>= 2) of M-point row teams.
+template <typename T, int N1, int M>
+constexpr bool alg1_valid() {
+  return rows_per_tile<N1, M, T>() >= 2 && rows_per_tile<N1, M, T>() % 2 == 0;
+}
+template <typename T, int N1, int M>
+cudaError_t alg1_check() {
+  return alg1_valid<T, N1, M>() ? cudaSuccess : cudaErrorNotSupported;
+}
+
+template <typename T, int N1, int M>
+cudaError_t launch_fused_alg1_impl(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out,
+                                   int64_t stride, cudaStream_t s);
+
 template <typename T, int N1, int M>
 cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out, int64_t stride,
                               cudaStream_t s) {
+  if constexpr (!alg1_valid<T, N1, M>()) {
+    return cudaErrorNotSupported;
+  } else {
+    return launch_fused_alg1_impl<T, N1, M>(f, seed, field0, nf, out, stride, s);
+  }
+}
+
+template <typename T, int N1, int M>
+cudaError_t launch_fused_alg1_impl(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out,
+                                   int64_t stride, cudaStream_t s) {
   using C = C_t<T>;
   constexpr int NT = fused_threads<N1, M, T>(), RPT = rows_per_tile<N1, M, T>();
   constexpr size_t smem = fused_smem<N1, M, T>();

@@ -34,7 +34,15 @@ GRFC_FUSED_PRE(512)
 GRFC_FUSED_PRE(1024)
 GRFC_FUSED_PRE(2048)
 #endif
-// Algorithm 1 (three-tile persistent kernel): square grids, M = N1/2.
-template cudaError_t launch_fused_alg1<INST_T, INST_N, INST_N / 2>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,
-                                                                  int64_t, cudaStream_t);
+// Algorithm 1 (three-tile persistent kernel): every (N1, M) whose row tiles hold
+// an even number of rows (alg1_valid); the others return cudaErrorNotSupported.
+#define GRFC_ALG1(M)                                                                                            \
+  template cudaError_t launch_fused_alg1<INST_T, INST_N, M>(const Fast2D&, uint64_t, uint64_t, int64_t, void*,   \
+                                                             int64_t, cudaStream_t);                             \
+  template cudaError_t alg1_check<INST_T, INST_N, M>();
+GRFC_ALG1(128)
+GRFC_ALG1(256)
+GRFC_ALG1(512)
+GRFC_ALG1(1024)
+GRFC_ALG1(2048)
 }  // namespace grfc

@@ -31,6 +31,8 @@ cudaError_t cluster_query(Fast2D& f, int cs, int nsl);
 template <typename T, int N1, int M>
 cudaError_t launch_fused_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out, int64_t stride,
                               cudaStream_t s);
+template <typename T, int N1, int M>
+cudaError_t alg1_check();
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 
@@ -39,7 +41,6 @@ bool fast2d_supported(int d, const int64_t* n, int dtype, int alg, int family) {
   (void)family;
   if (d != 2) return false;
   if (!is_pow2(n[0]) || !is_pow2(n[1])) return false;
-  if (alg == GRFC_TWO_FFT && n[0] != n[1]) return false;  // fused Algorithm 1: square grids
   return n[0] >= 256 && n[0] <= 4096 && n[1] >= 256 && n[1] <= 4096;
 }
 
@@ -111,15 +112,13 @@ static cudaError_t dispatch_rows(const Fast2D& f, int64_t nf, const void* W, voi
 template <typename T>
 static cudaError_t dispatch_alg1(const Fast2D& f, uint64_t seed, uint64_t field0, int64_t nf, void* out,
                                  int64_t stride, cudaStream_t s) {
-  if (f.n2 != f.n1) return cudaErrorNotSupported;
-  switch (f.n1) {
-    case 256: return GRFC_CALL_ALG1(T, 256, 128, 0);
-    case 512: return GRFC_CALL_ALG1(T, 512, 256, 0);
-    case 1024: return GRFC_CALL_ALG1(T, 1024, 512, 0);
-    case 2048: return GRFC_CALL_ALG1(T, 2048, 1024, 0);
-    case 4096: return GRFC_CALL_ALG1(T, 4096, 2048, 0);
-  }
-  return cudaErrorNotSupported;
+  GRFC_DISPATCH_N1(T, 0, GRFC_CALL_ALG1)
+}
+
+#define GRFC_CALL_ALG1_CHECK(T, N1, M, ALG) alg1_check<T, N1, M>()
+template <typename T>
+static cudaError_t dispatch_alg1_check(const Fast2D& f) {
+  GRFC_DISPATCH_N1(T, 0, GRFC_CALL_ALG1_CHECK)
 }
 
 template <typename T, int ALG>
@@ -189,6 +188,10 @@ cudaError_t fast2d_init(Fast2D& f, const GridDesc& g, const DensityDesc& D, int 
   f.n2 = (int)g.n[1];
   f.dtype = dtype;
   f.alg = alg;
+  if (alg == GRFC_TWO_FFT) {  // (N1, M) pairs without a fused Algorithm-1 kernel: generic path
+    const cudaError_t ok = dtype == GRFC_F64 ? dispatch_alg1_check<double>(f) : dispatch_alg1_check<float>(f);
+    if (ok != cudaSuccess) return cudaErrorNotSupported;
+  }
   f.g = g;
   f.D = D;
   f.s_one = s_one;
