@@ -7,6 +7,7 @@ sharing the GPU changes timing only."""
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -39,7 +40,7 @@ def _worker(rank, world, port, q):
     out = torch.empty(pts, dtype=torch.float32, device="cuda")
     plan.slab_pass_b(world, recv.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
-    q.put((rank, out.cpu()))
+    q.put((rank, out.cpu().numpy()))  # by value: a shared-memory tensor would die with this process
     dist.barrier()
     dist.destroy_process_group()
 
@@ -57,7 +58,7 @@ def test_slab_kernels_world2_gloo_bit_identical():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    field = torch.cat([got[r] for r in range(world)]).reshape(COUNTS)
+    field = torch.from_numpy(np.concatenate([got[r] for r in range(world)])).reshape(COUNTS)
     plan = grfc.Plan(COUNTS, (1.0, 1.0, 1.0), grfc.Density.gaussian_cov(3, 0.03), grfc.ONE_FFT_OVERWRITE, grfc.F32)
     want = plan.generate_tensor(9, 2, 1)[0].cpu()
     assert torch.equal(field, want)
