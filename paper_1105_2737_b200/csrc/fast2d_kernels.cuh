@@ -466,10 +466,22 @@ struct F2Params {
 // sqrt(g) at the cell (k1, k2) of the half-lattice. fp32 Matern/Gaussian use
 // float parameters and the SFU (ex2/lg2); everything else the generic
 // device evaluation (double inside).
-template <typename T>
+// Density kinds the fp32 fused kernels are specialised on: the two families
+// with SFU forms get kernels without any other family's code (no fp64
+// fallbacks, no per-cell family selects: c2 0.925 -> 0.894 ms); kDensAny
+// evaluates every family (runtime switch), and is the only kind for fp64.
+constexpr int kDensAny = 0, kDensMatern = 1, kDensGauss = 2;
+
+template <typename T, int DK = kDensAny>
 __device__ __forceinline__ T sqrt_g2(const F2Params& p, int k1, int k2) {
   const int k1w = k1 <= p.n1 / 2 ? k1 : k1 - p.n1;
   const int k2w = k2 <= p.n2 / 2 ? k2 : k2 - p.n2;
+  if constexpr (sizeof(T) == 4 && DK != kDensAny) {
+    const float w1 = (float)k1w * p.f_wstep1, w2 = (float)k2w * p.f_wstep2;
+    const float q = w1 * w1 + w2 * w2;
+    if constexpr (DK == kDensGauss) return p.f_sqrt_c * ex2_approx(p.f_gauss_k * q);
+    return p.f_sqrt_c * ex2_approx(p.f_nhalf_alpha * lg2_approx(1.0f + p.f_ell2 * q));
+  }
   if constexpr (sizeof(T) == 4) {
     if (p.family == GRFC_DENSITY_MATERN || p.family == GRFC_DENSITY_GAUSSIAN_COV) {
       const float w1 = (float)k1w * p.f_wstep1, w2 = (float)k2w * p.f_wstep2;
@@ -492,7 +504,7 @@ __device__ __forceinline__ T sqrt_g2(const F2Params& p, int k1, int k2) {
 // X(K) = conj(w(K)) sqrt(g) scale for a half-lattice cell with the Philox
 // stream: the overwrite (Alg 2) / exact-set (Alg 3) rules of
 // philox_cell_noise (generic.cu) specialised to 2D, one Philox call per cell.
-template <typename T, int ALG>
+template <typename T, int ALG, int DK = kDensAny>
 __device__ __forceinline__ C_t<T> gen_cell(const F2Params& p, int k1, int k2, const PhiloxKey& key, uint64_t field) {
   using C = C_t<T>;
   const T r = (T)0.70710678118654752440;
@@ -514,7 +526,7 @@ __device__ __forceinline__ C_t<T> gen_cell(const F2Params& p, int k1, int k2, co
   }
   T z0, z1;
   unit_pair<T>(key, field, u, p.uh, z0, z1);
-  const T mlt = sqrt_g2<T>(p, k1, k2) * (T)p.scale;
+  const T mlt = sqrt_g2<T, DK>(p, k1, k2) * (T)p.scale;
   if (self) return mk<C>(z0 * mlt, (T)0);
   const T wy = conj ? -r * z1 : r * z1;
   return mk<C>(r * z0 * mlt, -wy * mlt);
@@ -667,7 +679,8 @@ struct NoHook {
 // scheduler checks the next tile's dependency there, off the critical path.
 // `pre` runs on every thread after the column FFT and before the W stores (the
 // cluster scheduler waits there for the W slot to be free).
-template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook, bool PERM = false>
+template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook, bool PERM = false,
+          int DK = kDensAny>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
@@ -713,7 +726,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       }
       gslot(k1) = x;
     }
-  } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && p.sg) {
+  } else if (DK == kDensAny && ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && p.sg) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one Philox
     // call; sqrt(g) scale / sqrt 2 from the plan's per-cell table (L2-resident)
     const float* __restrict__ sgc = p.sg + col;
@@ -737,7 +750,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     const int k2w = col <= p.n2 / 2 ? col : col - p.n2;
     const float w2 = (float)k2w * p.f_wstep2;
     const float K = p.f_sqrt_c * p.f_scale * 0.70710678118654752440f;
-    const bool matern = p.family == GRFC_DENSITY_MATERN;
+    const bool matern = DK == kDensMatern || (DK == kDensAny && p.family == GRFC_DENSITY_MATERN);
     const float A = 1.0f + p.f_ell2 * w2 * w2, B = K * ex2_approx(p.f_gauss_k * w2 * w2);
 #pragma unroll (kGenUnroll)
     for (int t = 0; t < E / 2; ++t) {
@@ -754,14 +767,14 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       gslot(k1) = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
       gslot(k1 + N1 / 2) = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
     }
-  } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
+  } else if (DK == kDensAny && ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed) {
     const T r = (T)0.70710678118654752440, sc = (T)p.scale;
 #pragma unroll 1
     for (int t = 0; t < E / 2; ++t) {
       const int k1 = j + t * TT;
       float a0, b0, a1, b1;
       unit_quad_f32(key, fld, (uint64_t)((uint32_t)k1 * p.hd + col), a0, b0, a1, b1);
-      const T m0 = sqrt_g2<T>(p, k1, col) * sc * r, m1 = sqrt_g2<T>(p, k1 + N1 / 2, col) * sc * r;
+      const T m0 = sqrt_g2<T, DK>(p, k1, col) * sc * r, m1 = sqrt_g2<T, DK>(p, k1 + N1 / 2, col) * sc * r;
       gslot(k1) = mk<C>((T)a0 * m0, -(T)b0 * m0);
       gslot(k1 + N1 / 2) = mk<C>((T)a1 * m1, -(T)b1 * m1);
     }
@@ -769,9 +782,9 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
 #pragma unroll(kGen64Unroll)
     for (int t = 0; t < E; ++t) {
       const int k1 = j + t * TT;
-      C x = gen_cell<T, ALG>(p, k1, col, key, fld);
+      C x = gen_cell<T, ALG, DK>(p, k1, col, key, fld);
       if (packed) {  // column 0 + i * column M
-        const C y = gen_cell<T, ALG>(p, k1, p.m, key, fld);
+        const C y = gen_cell<T, ALG, DK>(p, k1, p.m, key, fld);
         x = mk<C>(x.x - y.y, x.y + y.x);
       }
       gslot(k1) = x;
@@ -1058,7 +1071,7 @@ constexpr int fused_min_blocks() {
          : (N1 == 1024 && sizeof(T) == 4 && ColPlan<N1, T>::X == 4) ? GRFC_FUSED1024_MINB
                                                                     : 0;
 }
-template <typename T, int N1, int M, int ALG>
+template <typename T, int N1, int M, int ALG, int DK = kDensAny>
 __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1, M, T>())
     k_fused2d(F2Params p, F2Sched q, PhiloxKey key, uint64_t field0, C_t<T>* __restrict__ ring, T* __restrict__ out,
               int64_t out_stride, const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2) {
@@ -1240,7 +1253,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     };
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
-      col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0)>(
+      col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK>(
           p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
           GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr, hook, t16);
       done_ctr = &q.col_done[m.slot];
@@ -1489,6 +1502,14 @@ cudaError_t fused_query(Fast2D& f) {
   constexpr size_t smem = fused_smem<N1, M, T>();
   cudaError_t e = cudaFuncSetAttribute(k_fused2d<T, N1, M, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if constexpr (sizeof(T) == 4 && ALG == GRFC_ONE_FFT_OVERWRITE) {
+    e = cudaFuncSetAttribute(k_fused2d<T, N1, M, ALG, kDensMatern>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_fused2d<T, N1, M, ALG, kDensGauss>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   int occ = 0, dev = 0, sms = 148;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<T, N1, M, ALG>, NT, smem);
   if (e != cudaSuccess) return e;
@@ -1563,7 +1584,25 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   q.stats = dstats;
   {
     LaunchScope ls("fused2d_persistent", s);
-    k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out, stride, tw1, tw2);
+    // fp32 Matern / Gaussian (no sqrt(g) table): the family-specialised kernel
+    const int dk = (sizeof(T) == 4 && ALG == GRFC_ONE_FFT_OVERWRITE && !f.d_sg)
+                       ? (f.D.family == GRFC_DENSITY_MATERN ? kDensMatern
+                          : f.D.family == GRFC_DENSITY_GAUSSIAN_COV ? kDensGauss : kDensAny)
+                       : kDensAny;
+    if constexpr (sizeof(T) == 4 && ALG == GRFC_ONE_FFT_OVERWRITE) {
+      if (dk == kDensMatern)
+        k_fused2d<T, N1, M, ALG, kDensMatern><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out,
+                                                                      stride, tw1, tw2);
+      else if (dk == kDensGauss)
+        k_fused2d<T, N1, M, ALG, kDensGauss><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out,
+                                                                     stride, tw1, tw2);
+      else
+        k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out, stride, tw1,
+                                                        tw2);
+    } else {
+      k_fused2d<T, N1, M, ALG><<<grid, NT, smem, s>>>(prm, q, philox_key(seed), field0, ring, (T*)out, stride, tw1,
+                                                      tw2);
+    }
   }
   e = cudaGetLastError();
   if (dstats) {
