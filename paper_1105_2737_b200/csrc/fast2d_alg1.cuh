@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RPT = rows_per_tile<N1, M, T>();
   __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
-  const C_t<T>* t16 = init_tw16<T>(s_tw16);
+  const C_t<T>* t16 = init_tw16<T>(s_tw16, tw2, 2 * M);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t L = q.L, F = q.F, g1 = q.g1, gc = q.gc, g2 = q.g2;
   // ticket ranges (L <= F/2): [0,L): R1 | [L,2L): R1 C | [2L,F): R1 C R2 | [F,F+L): C R2 | [F+L,F+2L): R2

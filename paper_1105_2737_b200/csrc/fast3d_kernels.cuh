@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1,
   __shared__ uint32_t s_ticket;
   constexpr int RPT = rows_per_tile<N1, M, T>();
   __shared__ C_t<T> s_tw16[GRFC_TW16 && sizeof(T) == 4 ? 240 : 1];
-  const C_t<T>* t16 = init_tw16<T>(s_tw16);
+  const C_t<T>* t16 = init_tw16<T>(s_tw16, tw2, 2 * M);
   const uint64_t slot_elems = (uint64_t)N1 * M;
   const uint32_t G = q.strips + q.rtiles, pro = q.L * q.strips, nfull = q.F - q.L;
   const uint32_t total = q.F * G;
