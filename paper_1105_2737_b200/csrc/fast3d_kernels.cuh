@@ -265,14 +265,29 @@ __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int
   const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
   const int col = s * SLOTS + slot;
   C v[E];
+  if (n1_per == N1) {
+    // one rank: the plane is one contiguous [k1][k] block — one pointer, and with
+    // the compile-time m of the persistent kernel every load is pointer + immediate
+    const C* __restrict__ b0 = src + ((int64_t)j0l * N1 + j) * m + col;
 #pragma unroll
-  for (int b = 0; b < E / R0; ++b)
+    for (int b = 0; b < E / R0; ++b)
 #pragma unroll
-    for (int i = 0; i < R0; ++i) {
-      const int k1 = j + b * TT + i * (N1 / R0);
-      const int r = k1 / n1_per, k1l = k1 - r * n1_per;
-      v[b * R0 + i] = __ldcs(&src[(((int64_t)r * n0_per + j0l) * n1_per + k1l) * m + col]);
-    }
+      for (int i = 0; i < R0; ++i) v[b * R0 + i] = __ldcs(b0 + (int64_t)(b * TT + i * (N1 / R0)) * m);
+  } else {
+    // slab blocks: row k1 lives in the block of rank k1 / n1_per (n1_per = N1 /
+    // world is a power of two: shifts and masks, no integer division)
+    // (32-bit element offsets: a rank's receive buffer holds < 2^31 elements for
+    // every pow2-3d plan, N <= 1024)
+    const int sh = __ffs(n1_per) - 1;
+#pragma unroll
+    for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+      for (int i = 0; i < R0; ++i) {
+        const uint32_t k1 = (uint32_t)(j + b * TT + i * (N1 / R0));
+        const uint32_t r = k1 >> sh, k1l = k1 & (uint32_t)(n1_per - 1);
+        v[b * R0 + i] = __ldcs(&src[((r * (uint32_t)n0_per + (uint32_t)j0l) * (uint32_t)n1_per + k1l) * (uint32_t)m + col]);
+      }
+  }
   std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{reinterpret_cast<C*>(smem_raw), slot};
   if constexpr (HasTw16<decltype(ex)>::value) ex.tw16 = t16;
   line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
