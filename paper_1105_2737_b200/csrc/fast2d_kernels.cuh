@@ -1017,6 +1017,12 @@ struct F2Sched {
   // per group; F_total is the batch. groups == 1: one queue over the grid.
   uint32_t groups, gsize, ctr_stride, F_total;
   uint64_t ring_stride;
+  // Deferral schedule (GRFC_DEFER): tickets interleave a field's column and row
+  // tiles (C(f+L, i), R(f, i) alternating) and a CTA whose next ticket is a row
+  // tile that is not ready yet parks it and runs its following ticket first
+  // (see k_fused2d): waits become column work, so a short L2-resident ring
+  // (small L, S) no longer stalls the queue.
+  uint32_t defer;
 };
 
 // Ring-slot division of the tile decoder (thread 0, once per tile).
@@ -1033,6 +1039,20 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Dependency-counter loads of the persistent 2D scheduler. GRFC_ACQ = 1: ld.acquire.gpu
+// (LDG.STRONG + CCTL.IVALL: the issuing thread blocks for the round trip, and the
+// invalidate empties the SM's L1 — the twiddle tables of all four resident CTAs — once
+// per tile). GRFC_ACQ = 0 (default): ld.relaxed.gpu, non-blocking until its value is
+// used at the end of the tile. W is only ever read with ld.global.cg (L2, never L1), by
+// threads that pass a CTA barrier after thread 0 has seen the producers' release
+// increments (red.release.gpu after their W stores), so no L1 invalidation is needed.
+#ifndef GRFC_ACQ
+#define GRFC_ACQ 0
+#endif
+__device__ __forceinline__ uint32_t dep_load(const uint32_t* p) {
+  return GRFC_ACQ ? ld_acquire_u32(p) : ld_relaxed_u32(p);
 }
 
 // Thread 0 polls with relaxed loads (no L1 invalidation per poll), then one
@@ -1055,6 +1075,9 @@ __device__ __forceinline__ void signal_done(uint32_t* ctr) {
 // tuned for the c2 shape (fp32 512 columns: 4 x 256 threads at 64 registers,
 // no spills; 3 CTAs at 80 registers measured 2% slower); other shapes let
 // ptxas choose.
+#ifndef GRFC_DEFER_BUILD
+#define GRFC_DEFER_BUILD 0
+#endif
 #ifndef GRFC_MID_CHECK
 #define GRFC_MID_CHECK 1
 #endif
@@ -1130,9 +1153,16 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
       x.idx = t % STRIPS;
     } else if ((t -= pro) < nfull * G) {
       const uint32_t g = t / G, r = t % G;
-      x.col = r < STRIPS;
+      if ((GRFC_DEFER_BUILD & 1) && q.defer) {
+        // proportional interleave of the group's STRIPS column and RT row tiles
+        const uint32_t rb = r * RT / G, ra = (r + 1) * RT / G;  // row tiles before / through position r
+        x.col = ra == rb;
+        x.idx = x.col ? r - rb : rb;
+      } else {
+        x.col = r < STRIPS;
+        x.idx = x.col ? r : r - STRIPS;
+      }
       x.f = x.col ? g + q.L : g;
-      x.idx = x.col ? r : r - STRIPS;
     } else {
       t -= nfull * G;
       x.col = false;
@@ -1149,6 +1179,14 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
     return x.col ? (GRFC_COL_LATE_WAIT ? 0u : x.use * RT) : (x.use + 1) * STRIPS;
   };
+  // Deferral schedule: what must hold before the tile may START when its CTA keeps a
+  // parked row tile — for a column tile also its ring-slot dependency (normally
+  // checked late, inside the tile): a CTA never blocks inside a tile while it holds
+  // a parked row, so every wait points to a strictly smaller ticket (no cycles).
+  auto dep_start = [&](const Tile& x, const uint32_t*& ctr) -> uint32_t {
+    ctr = x.col ? &q.row_done[x.slot] : &q.col_done[x.slot];
+    return x.col ? x.use * RT : (x.use + 1) * STRIPS;
+  };
   // Thread 0 holds two reserved tickets: tA (the next tile) and tB (the one
   // after, its atomic in flight). At the start of each tile it issues a
   // relaxed load of tA's dependency counter, consumed at the end of the tile,
@@ -1162,8 +1200,32 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     uint64_t pf_off;  // element offset of the W rows of the tile after next (pf: it is a row tile)
   };
   __shared__ Msg s_msg;
+  const bool DEFER = GRFC_DEFER_BUILD && q.defer;
   uint32_t tA = total, tB = total, dep_v = 0;
-  auto claim = [&]() { return atomicAdd(q.ticket, 1u); };
+  // early dependency check of the next (row) tile: the 16 bytes around its counter,
+  // fetched asynchronously mid-tile (s_dep_idx = 1 + word index, 0: none pending)
+  __shared__ __align__(16) uint32_t s_dep[4];
+  __shared__ uint32_t s_dep_idx;
+  if (threadIdx.x == 0) s_dep_idx = 0;
+  // deferral schedule (q.defer), thread 0: tD = parked row ticket (kNone: none) with
+  // dvD = 1 + its dependency counter acquired mid-tile; haveA: tA is reserved and unused
+  constexpr uint32_t kNone = 0xffffffffu;
+  // (kept in shared memory: touched by thread 0 only, a few times per tile, and the
+  // kernel sits at its 64-register budget)
+  __shared__ uint32_t s_tD, s_dvD, s_haveA;
+  if (threadIdx.x == 0) s_tD = kNone, s_dvD = 0, s_haveA = 0;
+  volatile uint32_t& tD = s_tD;
+  volatile uint32_t& dvD = s_dvD;
+  volatile uint32_t& haveA = s_haveA;
+  // The ticket atomic in inline PTX: a plain atomicAdd in thread 0's branch is
+  // warp-aggregated by the compiler (vote + shuffle of the returned value), and the
+  // shuffle waits for the atomic's round trip right there — warp 0 lost ~1k cycles at
+  // the top of every tile. The asm result is first read at the end of the tile.
+  auto claim = [&]() {
+    uint32_t t;
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(q.ticket) : "memory");
+    return t;
+  };
   // thread 0: message for ticket t (readiness from the early counter value v)
   // plus the prefetch target of ticket t2
   auto publish = [&](uint32_t t, uint32_t v, uint32_t t2) {
@@ -1180,7 +1242,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
           // v = 1 + the value acquired mid-tile (0: none); else one round trip here,
           // the acquire load both checking and ordering
           m.ready = v > target;
-          if (!m.ready) m.ready = ld_acquire_u32(ctr) >= target;
+          if (!m.ready) m.ready = dep_load(ctr) >= target;
         } else {
           if (v < target) v = ld_relaxed_u32(ctr);
           m.ready = v >= target;
@@ -1215,18 +1277,26 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
   for (;;) {
     long long t0 = STATS ? clock64() : 0;
     const Msg m = s_msg;
+    // (the exit test comes first: with the claim in front of it ptxas threaded
+    // thread 0's exit out of the middle of its divergent block, and the warp then
+    // reached the tile's aligned barriers unconverged: garbage fields)
+    if (m.t >= total) break;
     if (threadIdx.x == 0) {
-      if (GRFC_RES1) {
+      if ((GRFC_DEFER_BUILD & 2) && DEFER) {
+        if (!haveA) {
+          tA = claim();
+          haveA = 1u;
+        }
+      } else if (GRFC_RES1) {
         // GRFC_RES1: one reservation — the next tile's ticket is claimed now and
         // read at the end of this tile (its round trip hides behind the tile)
-        if (m.t < total) tA = claim();
+        tA = claim();
       } else if (tA < total) {  // early dependency load of the next tile
         const uint32_t* ctr;
         dep_of(decode(tA), ctr);
         dep_v = ld_relaxed_u32(ctr);
       }
     }
-    if (m.t >= total) break;
     if (m.pf) {
       // the tile after this one is a row tile: pull its W rows toward L2 now
       // (one 128-byte line per thread and pass); the ring is larger than L2
@@ -1242,7 +1312,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
         const uint32_t* ctr;
         const uint32_t target = dep_of(decode(m.t), ctr);
         while (ld_relaxed_u32(ctr) < target) __nanosleep(256);
-        if (!m.col) (void)ld_acquire_u32(ctr);
+        if (GRFC_ACQ && !m.col) (void)ld_acquire_u32(ctr);
       }
       __syncthreads();
     }
@@ -1254,10 +1324,29 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     // is read now with acquire semantics (ordering the CTA's later W reads after
     // the producers' releases), so publish() needs no round trip when it is met.
     auto hook = [&]() {
+      if ((GRFC_DEFER_BUILD & 4) && DEFER && tD != kNone) {  // the parked row tile's columns: done by now?
+        const uint32_t* ctr;
+        dep_of(decode(tD), ctr);
+        dvD = ld_acquire_u32(ctr) + 1u;
+      }
       if (GRFC_RES1 && GRFC_MID_CHECK && tA < total) {
         const Tile y = decode(tA);
         const uint32_t* ctr;
-        if (!y.col && dep_of(y, ctr)) dep_v = ld_acquire_u32(ctr) + 1u;  // +1: "acquired" marker
+        if (!y.col && dep_of(y, ctr)) {
+          if (GRFC_ACQ) {
+            dep_v = ld_acquire_u32(ctr) + 1u;  // +1: "acquired" marker
+          } else {
+            // cp.async (L2 -> shared, no destination register): thread 0 does not wait
+            // here, and nothing stays live in a register across the tile; the aligned
+            // 16 bytes around the counter are copied and publish() picks the word
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_dep);
+            const uint64_t ga = (uint64_t)ctr & ~15ull;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(ga) : "memory");
+            s_dep_idx = 1u + (uint32_t)(((uint64_t)ctr >> 2) & 3u);
+          }
+        }
+        if ((GRFC_DEFER_BUILD & 4) && DEFER && y.col && tD != kNone && dep_start(y, ctr))
+          dep_v = ld_relaxed_u32(ctr) + 1u;
       }
     };
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
@@ -1275,7 +1364,55 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     // every tile has internal barriers, so all threads have read s_msg
     long long e = STATS ? clock64() : 0;
     if (threadIdx.x == 0) {
-      if (GRFC_RES1) {
+      if ((GRFC_DEFER_BUILD & 8) && DEFER) {
+        // Next tile: the parked row if its columns are done; else the reserved ticket
+        // if it can run (a column tile, or a row tile that is ready); else park the
+        // reserved row and take the following ticket (interleaved order: a column
+        // tile); only when two unready rows are held does the CTA wait (for the older).
+        uint32_t next = total, v = 0;
+        bool picked = false;
+        const uint32_t* ctr;
+        if (tD != kNone) {
+          const uint32_t target = dep_of(decode(tD), ctr);
+          if (!dvD) dvD = ld_acquire_u32(ctr) + 1u;
+          if (dvD > target) {
+            next = tD, v = dvD, tD = kNone, picked = true;
+          }
+        }
+        // can ticket y start now? (vy = 1 + its counter if already loaded, else 0)
+        auto can_start = [&](const Tile& y, uint32_t& vy) {
+          const bool parked = tD != kNone;
+          if (y.col && !parked) return true;  // slot dependency checked late, inside the tile
+          const uint32_t target = dep_start(y, ctr);
+          if (!target) return true;
+          if (!vy) vy = (y.col ? ld_relaxed_u32(ctr) : ld_acquire_u32(ctr)) + 1u;
+          return vy > target;
+        };
+        if (!picked && haveA && tA < total) {
+          const Tile a = decode(tA);
+          uint32_t va = dep_v;
+          if (can_start(a, va)) {
+            next = tA, v = a.col ? 0u : va, haveA = 0u, picked = true;
+          } else if (tD == kNone) {  // an unready row: park it, take the following ticket
+            tD = tA;
+            tA = claim();
+            if (tA < total) {
+              const Tile b = decode(tA);
+              uint32_t vb = 0;
+              if (can_start(b, vb)) next = tA, v = b.col ? 0u : vb, haveA = 0u, picked = true;
+            }
+          }
+        }
+        if (!picked && tD != kNone) next = tD, v = 0, tD = kNone;  // waits in the next iteration
+        publish(next, v, total);
+        dep_v = 0;
+        dvD = 0;
+      } else if (GRFC_RES1) {
+        if (!GRFC_ACQ && s_dep_idx) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          dep_v = ((volatile uint32_t*)s_dep)[s_dep_idx - 1u] + 1u;
+          s_dep_idx = 0;
+        }
         publish(tA < total ? tA : total, dep_v, total);
         dep_v = 0;
       } else {
@@ -1573,6 +1710,7 @@ cudaError_t launch_fused(const Fast2D& f, uint64_t seed, uint64_t field0, int64_
   q.s_magic = slot_magic(q.F, q.S);
   q.ctr_stride = (uint32_t)(fused_ctr_bytes(q.S) / sizeof(uint32_t));
   q.ring_stride = (uint64_t)q.S * N1 * M;
+  if (const char* se = std::getenv("GRFC_DEFER")) q.defer = se[0] == '1';
   uint32_t* ctr = (uint32_t*)ws;  // per group: [ticket][col_done S][row_done S] (padded) | rings
   q.ticket = ctr;
   q.col_done = ctr + 1;

@@ -30,32 +30,34 @@ def make_density(c):
 
 
 def run(cfg, env, iters, alg):
+    # the overrides stay set for the whole variant: some switches are read at plan
+    # creation, others (ring geometry, schedule) at every launch
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
         c = bench.CONFIGS[cfg]
         plan = grfc.Plan(c["counts"], tuple(1.0 for _ in c["counts"]), make_density(c), alg,
                          grfc.F32 if c["dtype"] == "f32" else grfc.F64, device=0)
+        n = c["fields"]
+        out = plan.generate_tensor(0, 0, n)
+        for _ in range(3):
+            plan.generate_tensor(0, 0, n, out=out)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            plan.generate_tensor(0, 0, n, out=out)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts), out, plan.path
     finally:
         for k, v in saved.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    n = c["fields"]
-    out = plan.generate_tensor(0, 0, n)
-    for _ in range(3):
-        plan.generate_tensor(0, 0, n, out=out)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(iters):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        plan.generate_tensor(0, 0, n, out=out)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    return statistics.median(ts), out, plan.path
 
 
 def main():
