@@ -595,9 +595,26 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
+// Column tiles that may generate in registers (col_tile REGTILE): fp32 Algorithm 2,
+// one stage-0 butterfly per thread, shared-memory (not per-warp-region) exchange.
+template <typename T, int N1, int ALG>
+constexpr bool col_reggen_ok();
+
 // Column tile: one (field, strip) — 2*CB column FFTs of length N1 with
 // generation fused in front and the Z epilogue behind. Block = col_threads.
 // generation loop unroll of the fp32 column tiles (independent Philox chains in flight)
+#ifndef GRFC_REGGEN
+#define GRFC_REGGEN 1
+#endif
+#ifndef GRFC_REGGEN_GROUP
+#define GRFC_REGGEN_GROUP 4
+#endif
+#ifndef GRFC_REGGEN_WCOL
+#define GRFC_REGGEN_WCOL 1
+#endif
+#ifndef GRFC_REGGEN_MAXE
+#define GRFC_REGGEN_MAXE 32
+#endif
 #ifndef GRFC_GEN_UNROLL
 #define GRFC_GEN_UNROLL 4
 #endif
@@ -636,6 +653,12 @@ template <typename T, int N1, int MC, bool PERM = false>
 __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                              const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
                                              int col, bool packed, bool mid);
+template <typename T, int N1, int ALG>
+constexpr bool col_reggen_ok() {
+  return GRFC_REGGEN && (GRFC_REGGEN_WCOL || !col_warp_mode<N1, T>()) && sizeof(T) == 4 &&
+         ALG == GRFC_ONE_FFT_OVERWRITE &&
+         ColPlan<N1, T>::E == RFirst<typename ColPlan<N1, T>::R>::value && ColPlan<N1, T>::E <= GRFC_REGGEN_MAXE;
+}
 
 // Strip-blocked W columns (PERM, the persistent kernels' long-column plans): the
 // column tile of strip s writes its 2CB columns {s CB + c} and {M - s CB - c}
@@ -689,7 +712,7 @@ struct NoHook {
 // `pre` runs on every thread after the column FFT and before the W stores (the
 // cluster scheduler waits there for the W slot to be free).
 template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook, bool PERM = false,
-          int DK = kDensAny>
+          int DK = kDensAny, bool REGTILE = false>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
@@ -720,6 +743,17 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // it is only needed before the W stores, so its latency hides behind the tile.
   uint32_t dep_seen = 0;
   if (dep && threadIdx.x == 0) dep_seen = ld_relaxed_u32(dep);
+  C v[E];
+  // REGGEN (fp32 Matern/Gaussian interior columns, one stage-0 butterfly per thread):
+  // the generation loop is fully unrolled and writes the stage-0 inputs straight into
+  // v (row j + t TT is input t) instead of staging them through shared memory — 2E
+  // shared-memory instructions per thread and one CTA barrier per tile less (the
+  // shared-memory data pipe is the busiest unit of the c2 kernel: 60% of peak).
+  // REGTILE is chosen per tile by the caller (col_reggen_ok; never strip 0, which holds
+  // the packed and middle columns and stages through shared memory as before): two
+  // copies of the tile code instead of a merge of both generation paths into one FFT
+  // (the merge made ptxas spill 280 bytes).
+  constexpr bool reg_tile = REGTILE;
   // GRFC_EARLY_REL: release the previous tile before generation (its consumers
   // wait on it; the fence stalls warp 0 only while the others generate)
   if (GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
@@ -750,6 +784,36 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
       gslot(k1) = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
       gslot(k1 + N1 / 2) = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
+    }
+  } else if constexpr (reg_tile) {
+    const int k2w = col <= p.n2 / 2 ? col : col - p.n2;
+    const float w2 = (float)k2w * p.f_wstep2;
+    const float K = p.f_sqrt_c * p.f_scale * 0.70710678118654752440f;
+    const bool matern = DK == kDensMatern || (DK == kDensAny && p.family == GRFC_DENSITY_MATERN);
+    const float A = 1.0f + p.f_ell2 * w2 * w2, B = K * ex2_approx(p.f_gauss_k * w2 * w2);
+    uint32_t u0 = (uint32_t)j * p.hd + col;
+    const uint32_t ustep = (uint32_t)TT * p.hd;
+#pragma unroll
+    for (int t = 0; t < E / 2; ++t) {
+      const int k1 = j + t * TT;
+      // groups of GRFC_REGGEN_GROUP independent Philox chains: the next group's counter
+      // is made to depend on every result of this one, or ptxas runs all E/2 chains
+      // at once and spills
+      if (t > 0 && t % GRFC_REGGEN_GROUP == 0) {
+#pragma unroll
+        for (int g = 1; g <= GRFC_REGGEN_GROUP; ++g)
+          asm volatile("" : "+r"(u0) : "f"(v[t - g].x), "f"(v[t - g].y), "f"(v[t - g + E / 2].x), "f"(v[t - g + E / 2].y));
+      }
+      const uint4 r = philox_draw(key, fld, (uint64_t)(u0 + (uint32_t)t * ustep));
+      float rad0, s0, c0, rad1, s1, c1;
+      box_muller_parts_f32(r.x, r.y, rad0, s0, c0);
+      box_muller_parts_f32(r.z, r.w, rad1, s1, c1);
+      const float q0 = rowq[k1], q1 = rowq[k1 + N1 / 2];
+      const float m0 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q0), p.f_lg2K)) : B * q0;
+      const float m1 = matern ? ex2_approx(__fmaf_rn(p.f_nhalf_alpha, lg2_approx(A + q1), p.f_lg2K)) : B * q1;
+      const float g0 = rad0 * m0, g1 = rad1 * m1;  // (rad m) (c, -s) = (z0 m, -z1 m)
+      v[t] = mk<C>((T)(g0 * c0), (T)(-g0 * s0));
+      v[t + E / 2] = mk<C>((T)(g1 * c1), (T)(-g1 * s1));
     }
   } else if (ALG == GRFC_ONE_FFT_OVERWRITE && sizeof(T) == 4 && !packed && rowq) {
     // interior column: rows k1 and k1 + N1/2 are units u and u + Uh — one
@@ -807,14 +871,15 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // so the fence in front of the increment is cheap (persistent kernel).
   if (!GRFC_EARLY_REL && sig && threadIdx.x == 0) red_release_add(sig, 1u);
   if (threadIdx.x == 0) hook();
-  C v[E];
+  if (!reg_tile) {
 #pragma unroll
-  for (int b = 0; b < E / R0; ++b)
+    for (int b = 0; b < E / R0; ++b)
 #pragma unroll
-    for (int i = 0; i < R0; ++i) v[b * R0 + i] = gslot(j + b * TT + i * (N1 / R0));
+      for (int i = 0; i < R0; ++i) v[b * R0 + i] = gslot(j + b * TT + i * (N1 / R0));
+  }
   if constexpr (WCOL) {
     RowEx<C, true, GTT == 32, (GTT > 32 ? GTT : 0)> wex{rg, true, 1 + slot};
-    wex.sync();  // own rows read back: the group's first exchange may overwrite them
+    if (!reg_tile) wex.sync();  // own rows read back: the group's first exchange may overwrite them
     line_fft<N1, E, +1>(v, j, tw1, 1, wex, typename PL::R{});
     // results to the region in natural row order, then one CTA barrier (thread 0
     // first checks the ring-slot reuse dependency: every W store follows it)
@@ -826,7 +891,9 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     pre();
     __syncthreads();
   } else {
-    __syncthreads();
+    // orders the read-back of staged rows before the first exchange's writes; with
+    // REGGEN only strip 0 (the packed column's threads) stages anything
+    if (!reg_tile) __syncthreads();
     using Ex = std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>>;
     Ex ex{sm, slot};
     if constexpr (HasTw16<Ex>::value) ex.tw16 = t16;
@@ -1351,9 +1418,16 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     };
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
-      col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK>(
-          p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr,
-          GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr, hook, t16);
+      // (a plan with a per-cell sqrt(g) table, p.sg, keeps the table path)
+      if (col_reggen_ok<T, N1, ALG>() && table && !p.sg && m.idx > 0)
+        col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK, col_reggen_ok<T, N1, ALG>()>(
+            p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw, s_rowq,
+            GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr, hook, t16);
+      else
+        col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK>(
+            p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw,
+            table ? s_rowq : nullptr, GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT,
+            done_ctr, hook, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
       row_tile<T, M, RPT, fused_threads<N1, M, T>(), decltype(hook), w_perm_cb<N1, T>()>(

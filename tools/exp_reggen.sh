@@ -3,8 +3,9 @@ cat > /tmp/a.py <<'PY'
 import os, sys, torch, statistics, hashlib
 sys.path.insert(0, '/root/repo')
 import bench
+CFGS = sys.argv[1:] or ['c2','c5','c3']
 from paper_1105_2737_b200 import grfc
-for cfg in ('c2','c5','c3'):
+for cfg in CFGS:
     c = bench.CONFIGS[cfg]
     fam = c["density"]; d = len(c["counts"])
     dens = grfc.Density.gaussian_cov(d, fam[1]) if fam[0] == "gauss" else grfc.Density.matern(d, fam[1], fam[2])
@@ -24,4 +25,6 @@ for cfg in ('c2','c5','c3'):
     h = hashlib.sha1(out[:: max(1, n//8)].contiguous().cpu().numpy().tobytes()).hexdigest()[:12]
     print(cfg, f"{ms:.4f} ms {pts/ms/1e6:.1f} Gpts/s min {min(ts):.4f} sha {h}", flush=True)
 PY
-for lib in paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xacq.so paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xacq.so; do echo "== $lib"; GRFC_LIB=$lib timeout 200 python /tmp/a.py 2>&1 | tail -3; done
+for lib in paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnow.so paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnow.so; do echo "== $lib"; GRFC_LIB=$lib timeout 100 python /tmp/a.py c3 2>&1 | tail -3; done
+GRFC_LIB=paper_1105_2737_b200/lib/libgrfc.so timeout 100 python /tmp/a.py c2 c5 2>&1 | tail -3
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
