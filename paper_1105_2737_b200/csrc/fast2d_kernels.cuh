@@ -606,6 +606,24 @@ constexpr bool col_reggen_ok();
 #ifndef GRFC_REGGEN
 #define GRFC_REGGEN 1
 #endif
+// SHF2: column plans <16, 16, 2> of 32-thread teams (fp32 512-point columns, c2): the
+// final radix-2 stage pairs team positions j and j ^ 16 on the same register index, so
+// with those two in one warp (lane bit 3) it runs on shuffles — each lane passes half of
+// its elements and computes both outputs of the others — instead of a second trip
+// through shared memory: 16 SHFL per thread for 16 STS + 16 LDS (64-bit: 64 -> 16
+// wavefronts of the shared-memory data pipe per warp) and two CTA barriers less.
+#ifndef GRFC_SHF2
+#define GRFC_SHF2 1
+#endif
+template <typename RS>
+struct IsR16_16_2 : std::false_type {};
+template <>
+struct IsR16_16_2<Radices<16, 16, 2>> : std::true_type {};
+template <int N1, typename T>
+constexpr bool col_shf2() {
+  return GRFC_SHF2 && sizeof(T) == 4 && N1 == 512 && IsR16_16_2<typename ColPlan<N1, T>::R>::value &&
+         ColPlan<N1, T>::E == 16 && ColPlan<N1, T>::X == 4;
+}
 #ifndef GRFC_REGGEN_GROUP
 #define GRFC_REGGEN_GROUP 4
 #endif
@@ -730,7 +748,13 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   constexpr bool WCOL = col_warp_mode<N1, T>();
   constexpr int GTT = N1 / E;  // threads per column group (one warp or several: named barrier)
   const int tid = threadIdx.x;
-  const int slot = WCOL ? tid / GTT : tid % SLOTS, j = WCOL ? tid % GTT : tid / SLOTS;
+  constexpr bool SHF2 = col_shf2<N1, T>();
+  static_assert(!SHF2 || (!col_warp_mode<N1, T>() && SLOTS == 8 && TT == 32), "SHF2 geometry");
+  // SHF2: lane = slot + 8 (j >> 4) + 16 (j & 1), warp = (j >> 1) & 7 — lanes across the
+  // strip's slots as before (coalesced W stores), j ^ 16 at lane ^ 8, and two even and
+  // two odd team positions per warp (the padded exchange rows stay spread over the banks)
+  const int slot = WCOL ? tid / GTT : tid % SLOTS;
+  const int j = WCOL ? tid % GTT : SHF2 ? (((tid >> 3) & 1) << 4) + ((tid >> 4) & 1) + ((tid >> 5) << 1) : tid / SLOTS;
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);
 
@@ -900,8 +924,32 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     // The slot's previous field must be consumed before W is overwritten: checked
     // at the FFT's exchange barriers (all W stores follow the last one).
     constexpr bool has_ex = RFirst<typename PL::R>::value != N1;
-    if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
-    line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    if constexpr (SHF2) {
+      ex.dep = LateDep{dep, dep_target, dep_seen, 1};  // checked at the (only) exchange's second barrier
+      run_stages<N1, E, +1, 1, 16, 16>(v, j, tw1, 1, ex);
+      // v[i] = stage-2 output 256 (j >> 4) + (j & 15) + 16 i; butterfly jj = (j & 15) + 16 i
+      // pairs it with position jj + 256 (lane ^ 8, same i), twiddle w_512^jj. Lane h =
+      // j >> 4 takes the butterflies with i = 2c + h: jj = j + 32 c, outputs rows jj
+      // and jj + 256 — the layout line_fft returns (v[2c + i'] = row j + 32 c + 256 i').
+      const bool h = (j >> 4) != 0;
+      const C wj = __ldg(&tw1[j]);
+      Unroll<0, 8>::run([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        const C snd = h ? v[2 * c] : v[2 * c + 1];
+        C rcv;
+        rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
+        rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
+        const C lo = h ? rcv : v[2 * c], hi = h ? v[2 * c + 1] : rcv;
+        constexpr T wc = (T)cos_2pi(c, 16), ws = (T)sin_2pi(c, 16);  // e^{2 pi i 32 c / 512}
+        const C w = c == 0 ? wj : cmul_cs(wj, wc, ws);
+        const C t = cmul(hi, w);
+        v[2 * c] = cadd(lo, t);
+        v[2 * c + 1] = csub(lo, t);
+      });
+    } else {
+      if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
+      line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+    }
     pre();
     if (dep && !has_ex) {
       if (threadIdx.x == 0 && dep_seen < dep_target)
