@@ -304,6 +304,57 @@ __device__ __forceinline__ void run_stages(C* v, int j, const C* __restrict__ tw
   }
 }
 
+// run_stages split at the last exchange: run_head runs every stage but the last and
+// ends with the puts of the last exchange (no barrier); run_tail gets the last stage's
+// inputs for team position j from `ex` (possibly another thread mapping and exchange
+// view than the head's) and runs it. head + barrier + tail == run_stages.
+template <int N, int E, int SIGN, int NS, int R, int... Rest, typename C, typename Ex>
+__device__ __forceinline__ void run_head(C* v, int j, const C* __restrict__ tw, int tws, Ex& ex) {
+  static_assert(sizeof...(Rest) > 0, "run_head needs an exchange");
+  stage_compute<N, E, R, NS, SIGN>(v, j, tw, tws, ex_tw16<C>(ex));
+  constexpr int TT = N / E;
+#pragma unroll
+  for (int b = 0; b < E / R; ++b) {
+    const int jj = j + b * TT;
+    const int base = (jj / NS) * NS * R + (jj % NS);
+    Unroll<0, R>::run([&](auto ii) {
+      constexpr int i = decltype(ii)::value;
+      ex_put<i * NS>(ex, base, v[b * R + i]);
+    });
+  }
+  if constexpr (sizeof...(Rest) > 1) {
+    constexpr int R2 = RFirst<Radices<Rest...>>::value;
+    ex.sync();
+#pragma unroll
+    for (int b = 0; b < E / R2; ++b) {
+      const int base = j + b * TT;
+      Unroll<0, R2>::run([&](auto ii) {
+        constexpr int i = decltype(ii)::value;
+        v[b * R2 + i] = ex_get<i * (N / R2), C>(ex, base);
+      });
+    }
+    ex.sync();
+    run_head<N, E, SIGN, NS * R, Rest...>(v, j, tw, tws, ex);
+  }
+}
+template <int N, int E, int SIGN, int RL, typename C, typename Ex>
+__device__ __forceinline__ void run_tail(C* v, int j, const C* __restrict__ tw, int tws, const Ex& ex) {
+  constexpr int TT = N / E;
+#pragma unroll
+  for (int b = 0; b < E / RL; ++b) {
+    const int base = j + b * TT;
+    Unroll<0, RL>::run([&](auto ii) {
+      constexpr int i = decltype(ii)::value;
+      v[b * RL + i] = ex_get<i * (N / RL), C>(ex, base);
+    });
+  }
+  stage_compute<N, E, RL, N / RL, SIGN>(v, j, tw, tws);
+}
+template <int N, int E, int SIGN, typename C, typename Ex, int... Rs>
+__device__ __forceinline__ void line_fft_head(C* v, int j, const C* __restrict__ tw, int tws, Ex& ex, Radices<Rs...>) {
+  run_head<N, E, SIGN, 1, Rs...>(v, j, tw, tws, ex);
+}
+
 template <typename RS>
 struct RNext;
 template <int R0, int R1, int... Rs>
@@ -627,6 +678,9 @@ constexpr bool col_shf2() {
 #ifndef GRFC_REGGEN_GROUP
 #define GRFC_REGGEN_GROUP 4
 #endif
+#ifndef GRFC_WTAIL
+#define GRFC_WTAIL 1
+#endif
 #ifndef GRFC_REGGEN_WCOL
 #define GRFC_REGGEN_WCOL 1
 #endif
@@ -904,16 +958,32 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   if constexpr (WCOL) {
     RowEx<C, true, GTT == 32, (GTT > 32 ? GTT : 0)> wex{rg, true, 1 + slot};
     if (!reg_tile) wex.sync();  // own rows read back: the group's first exchange may overwrite them
-    line_fft<N1, E, +1>(v, j, tw1, 1, wex, typename PL::R{});
-    // results to the region in natural row order, then one CTA barrier (thread 0
-    // first checks the ring-slot reuse dependency: every W store follows it)
+    if constexpr (GRFC_WTAIL && RCount<typename PL::R>::value > 1) {
+      // Every stage but the last in the column-group mapping; the last exchange's
+      // gets and the last stage run in the epilogue's slot-across-lanes mapping
+      // (slot = tid % SLOTS, j = tid / SLOTS), so the results are already where the
+      // W stores and the shuffle pairing want them: no transposing pass through
+      // shared memory (2E shared-memory instructions per thread less). The one CTA
+      // barrier between the two mappings also carries the ring-slot check.
+      line_fft_head<N1, E, +1>(v, j, tw1, 1, wex, typename PL::R{});
+      LateDep{dep, dep_target, dep_seen, 0}.check();
+      pre();
+      __syncthreads();
+      const int slot2 = tid % SLOTS, j2 = tid / SLOTS;
+      const RowEx<C, true> ex2{sm + slot2 * wcol_pitch(N1)};
+      run_tail<N1, E, +1, RL>(v, j2, tw1, 1, ex2);
+    } else {
+      line_fft<N1, E, +1>(v, j, tw1, 1, wex, typename PL::R{});
+      // results to the region in natural row order, then one CTA barrier (thread 0
+      // first checks the ring-slot reuse dependency: every W store follows it)
 #pragma unroll
-    for (int b = 0; b < E / RL; ++b)
+      for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-      for (int i = 0; i < RL; ++i) rg[RowEx<C>::pad(j + b * TT + i * (N1 / RL))] = v[b * RL + i];
-    LateDep{dep, dep_target, dep_seen, 0}.check();
-    pre();
-    __syncthreads();
+        for (int i = 0; i < RL; ++i) rg[RowEx<C>::pad(j + b * TT + i * (N1 / RL))] = v[b * RL + i];
+      LateDep{dep, dep_target, dep_seen, 0}.check();
+      pre();
+      __syncthreads();
+    }
   } else {
     // orders the read-back of staged rows before the first exchange's writes; with
     // REGGEN only strip 0 (the packed column's threads) stages anything
@@ -975,11 +1045,13 @@ __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* _
     slot = threadIdx.x % SLOTS;
     j = threadIdx.x / SLOTS;
     col = slot_column(s, slot, CB, p.m, packed, mid);
-    const C* rgs = sm + slot * wcol_pitch(N1);
+    if constexpr (!(GRFC_WTAIL && RCount<typename PL::R>::value > 1)) {  // else: the tail ran in this mapping
+      const C* rgs = sm + slot * wcol_pitch(N1);
 #pragma unroll
-    for (int b = 0; b < E / RL; ++b)
+      for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-      for (int i = 0; i < RL; ++i) v[b * RL + i] = rgs[RowEx<C>::pad(j + b * TT + i * (N1 / RL))];
+        for (int i = 0; i < RL; ++i) v[b * RL + i] = rgs[RowEx<C>::pad(j + b * TT + i * (N1 / RL))];
+    }
   }
   const C w = __ldg(&tw2[col]);  // e^{2 pi i col / N2}
   const bool special = packed || mid;

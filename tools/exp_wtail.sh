@@ -25,6 +25,5 @@ for cfg in CFGS:
     h = hashlib.sha1(out[:: max(1, n//8)].contiguous().cpu().numpy().tobytes()).hexdigest()[:12]
     print(cfg, f"{ms:.4f} ms {pts/ms/1e6:.1f} Gpts/s min {min(ts):.4f} sha {h}", flush=True)
 PY
-for lib in paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnow.so paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnow.so; do echo "== $lib"; GRFC_LIB=$lib timeout 100 python /tmp/a.py c3 2>&1 | tail -3; done
-GRFC_LIB=paper_1105_2737_b200/lib/libgrfc.so timeout 100 python /tmp/a.py c2 c5 2>&1 | tail -3
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+for lib in paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnowt.so paper_1105_2737_b200/lib/libgrfc.so paper_1105_2737_b200/build/libgrfc_xnowt.so; do echo "== $lib"; GRFC_LIB=$lib timeout 100 python /tmp/a.py c3 2>&1 | tail -3; done
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
