@@ -711,12 +711,15 @@ constexpr bool col_warp_mode() {
          2 * ColPlan<N1, T>::X <= 15 && 2 * ColPlan<N1, T>::X * (N1 / ColPlan<N1, T>::E) == col_threads<N1, T>();
 }
 // strip-blocked W (wpos) for the long-column plans of the persistent kernels
+#ifndef GRFC_WPERM_ALL
+#define GRFC_WPERM_ALL 1
+#endif
 #ifndef GRFC_WPERM
 #define GRFC_WPERM 1
 #endif
 template <int N1, typename T>
 constexpr int w_perm_cb() {
-  return (GRFC_WPERM && col_warp_mode<N1, T>()) ? ColPlan<N1, T>::X : 0;
+  return (GRFC_WPERM && (col_warp_mode<N1, T>() || (GRFC_WPERM_ALL && sizeof(T) == 4))) ? ColPlan<N1, T>::X : 0;
 }
 // per-column region: N1 padded rows + 4 elements (so the regions start 8 banks apart)
 constexpr int wcol_pitch(int n1) { return n1 + n1 / 16 + 4; }

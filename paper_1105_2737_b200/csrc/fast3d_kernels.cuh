@@ -52,6 +52,18 @@ GRFC_PLAN3(512, double, 16, 2, 16, 16, 2)
 GRFC_PLAN3(1024, double, 16, 2, 16, 16, 4)
 #undef GRFC_PLAN3
 
+// Strip-blocked W columns in 3D (as wpos in the 2D kernels): pass A stores the 2 CB
+// columns {s CB + c}, {M - s CB - c} of a (j0, k1) row as one contiguous run at
+// s 2CB + side CB + c; pass B's column tiles work on positions (the axis-1 FFT does not
+// depend on which column it holds) and its row tiles load through wpos.
+#ifndef GRFC_WPERM3
+#define GRFC_WPERM3 1
+#endif
+template <typename T>
+constexpr int w3_perm_cb() {
+  return (GRFC_WPERM3 && sizeof(T) == 4) ? 4 : 0;
+}
+
 template <int N0, typename T>
 constexpr int colgen3_threads() {
   return 4 * ColPlan3<N0, T>::X * (N0 / ColPlan3<N0, T>::E);
@@ -240,6 +252,8 @@ __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T
   } ex{sm, slot};
   line_fft<N0, E, +1>(v, j, tw0, 1, ex, typename PL::R{});
   const int kl = k1 - k1_lo;
+  static_assert(w3_perm_cb<T>() == 0 || w3_perm_cb<T>() == CB, "strip-blocked W needs the pass-A CB");
+  const int wcol = w3_perm_cb<T>() ? s * 2 * CB + side * CB + c : col;
   const bool store = kl >= 0 && kl < k1_cnt && !(h == 1 && k1 == a);  // h = 1 duplicates k1 in {0, N1/2}
   if (store) {
 #pragma unroll
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(colgen3_threads<N0, T>(), colgen3_min_blocks<T
 #pragma unroll
       for (int i = 0; i < RL; ++i) {
         const int j0 = j + b * TT + i * (N0 / RL);
-        W[((int64_t)j0 * k1_cnt + kl) * p.m + col] = v[b * RL + i];
+        W[((int64_t)j0 * k1_cnt + kl) * p.m + wcol] = v[b * RL + i];
       }
   }
 }
@@ -351,8 +365,8 @@ __global__ void __launch_bounds__(col_threads<N1, T>(), planes_min_blocks<T, N1,
       signal_done(&q.col_done[slot]);
     } else {
       wait_geq(&q.col_done[slot], (use + 1) * q.strips);
-      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw,
-                                                     nullptr, NoHook{}, t16);
+      row_tile<T, M, RPT, fused_threads<N1, M, T>(), NoHook, w3_perm_cb<T>()>(
+          Wp, (int)idx * RPT, N1, out + (int64_t)f * N1 * (2 * M), tw2, smem_raw, nullptr, NoHook{}, t16);
       signal_done(&q.row_done[slot]);
     }
   }

@@ -324,7 +324,8 @@ cudaError_t fast2d_generate(Fast2D& f, int alg, uint64_t seed, uint64_t field0, 
   if (alg == GRFC_TWO_FFT)  // Algorithm 1: always the persistent three-tile kernel
     return f.dtype == GRFC_F64 ? dispatch_alg1<double>(f, seed, field0, nf, out, stride, s)
                                : dispatch_alg1<float>(f, seed, field0, nf, out, stride, s);
-  if (f.persistent && f.dtype == GRFC_F64 && !f.cluster && nf * f.strips < f.sms) {
+  static const bool prex_on = !(std::getenv("GRFC_PREX") && std::getenv("GRFC_PREX")[0] == '0');  // A/B switch
+  if (prex_on && f.persistent && f.dtype == GRFC_F64 && !f.cluster && nf * f.strips < f.sms) {
     // a batch whose column tiles cannot fill the GPU (c1: one 512^2 field = 64
     // tiles): X(K) for every cell first, one cell per thread over all SMs
     // (k_gen_x2d), then the fused kernel with column tiles that load it (kPreX)
