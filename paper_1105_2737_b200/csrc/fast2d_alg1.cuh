@@ -35,6 +35,17 @@ __device__ __forceinline__ C_t<T> half_c(C_t<T> a) {
   return mk<C_t<T>>(a.x * (T)0.5, a.y * (T)0.5);
 }
 
+// Strip-blocked W columns (wpos) in the Algorithm-1 kernel: the C tile's loads and stores
+// of its 2 CB columns become one contiguous run per row; R1 stores and R2 loads go
+// through wpos.
+#ifndef GRFC_ALG1_WPERM
+#define GRFC_ALG1_WPERM 1
+#endif
+template <int N1, typename T>
+constexpr int alg1_perm_cb() {
+  return (GRFC_ALG1_WPERM && sizeof(T) == 4) ? ColPlan<N1, T>::X : 0;
+}
+
 // R1: rows r0 + p and r0 + p + N1/2 for p < RPT/2 (Philox pair sharing).
 template <typename T, int N1, int M, int RPT>
 __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int r0,
@@ -81,7 +92,7 @@ __device__ __forceinline__ void r1_tile(const F2Params& p, const PhiloxKey& key,
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-    for (int i = 0; i < RL; ++i) __stcg(&o[j + b * TT + i * (M / RL)], v[b * RL + i]);
+    for (int i = 0; i < RL; ++i) __stcg(&o[wpos(j + b * TT + i * (M / RL), M, alg1_perm_cb<N1, T>())], v[b * RL + i]);
 }
 
 // C: forward column FFT, spectral scaling, inverse pre-twiddle, column FFT.
@@ -98,13 +109,15 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);
   const int pcol = p.m - col;  // Zh partner column (for packed: M)
+  // strip-blocked W (wpos): this tile's 2 CB columns are one contiguous run per row
+  const int wcol = alg1_perm_cb<N1, T>() ? s * SLOTS + slot : col;
   C* sm = reinterpret_cast<C*>(smem_raw);
   const T half = (T)0.5;
   // 1. Zf columns -> smem [j1][slot]
 #pragma unroll 4
   for (int t = 0; t < E; ++t) {
     const int j1 = j + t * TT;
-    sm[j1 * SLOTS + slot] = __ldcg(&Wf[(int64_t)j1 * p.m + col]);
+    sm[j1 * SLOTS + slot] = __ldcg(&Wf[(int64_t)j1 * p.m + wcol]);
   }
   __syncthreads();
   if (sig && threadIdx.x == 0) red_release_add(sig, 1u);  // the CTA's previous tile
@@ -190,7 +203,7 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-    for (int i = 0; i < RL; ++i) __stcg(&Wf[(int64_t)(j + b * TT + i * (N1 / RL)) * p.m + col], v[b * RL + i]);
+    for (int i = 0; i < RL; ++i) __stcg(&Wf[(int64_t)(j + b * TT + i * (N1 / RL)) * p.m + wcol], v[b * RL + i]);
 }
 
 #ifndef GRFC_ALG1_RES1
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), alg1_min_blocks<N1,
       alg1_col_tile<T, N1>(p, (int)m.idx, Wf, tw1, tw2, smem_raw, done_ctr, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT, fused_threads<N1, M, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
+      row_tile<T, M, RPT, fused_threads<N1, M, T>(), NoHook, alg1_perm_cb<N1, T>()>(Wf, (int)m.idx * RPT, N1, out + (int64_t)m.f * out_stride, tw2,
                                                      smem_raw, done_ctr, NoHook{}, t16);
       done_ctr = &q.row_done[m.slot];
     }
