@@ -646,6 +646,33 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
+// SHF2 thread mapping and final stage (see col_shf2). tid -> team position j: lane =
+// slot + 8 (j >> 4) + 16 (j & 1), warp = (j >> 1) & 7.
+__device__ __forceinline__ int shf2_team_pos(int tid) { return (((tid >> 3) & 1) << 4) + ((tid >> 4) & 1) + ((tid >> 5) << 1); }
+// After run_stages<512, 16, +1, 1, 16, 16>: v[i] = stage-2 output 256 (j >> 4) + (j & 15) + 16 i.
+// Butterfly jj = (j & 15) + 16 i pairs it with position jj + 256 (lane ^ 8, same i), twiddle
+// w_512^jj. Lane h = j >> 4 takes the butterflies with i = 2c + h: jj = j + 32 c, outputs rows
+// jj and jj + 256 — the layout line_fft returns (v[2c + i'] = row j + 32 c + 256 i').
+template <typename T>
+__device__ __forceinline__ void shf2_stage(C_t<T>* v, int j, const C_t<T>* __restrict__ tw1) {
+  using C = C_t<T>;
+  const bool h = (j >> 4) != 0;
+  const C wj = __ldg(&tw1[j]);
+  Unroll<0, 8>::run([&](auto cc) {
+    constexpr int c = decltype(cc)::value;
+    const C snd = h ? v[2 * c] : v[2 * c + 1];
+    C rcv;
+    rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
+    rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
+    const C lo = h ? rcv : v[2 * c], hi = h ? v[2 * c + 1] : rcv;
+    constexpr T wc = (T)cos_2pi(c, 16), ws = (T)sin_2pi(c, 16);  // e^{2 pi i 32 c / 512}
+    const C w = c == 0 ? wj : cmul_cs(wj, wc, ws);
+    const C t = cmul(hi, w);
+    v[2 * c] = cadd(lo, t);
+    v[2 * c + 1] = csub(lo, t);
+  });
+}
+
 // Column tiles that may generate in registers (col_tile REGTILE): fp32 Algorithm 2,
 // one stage-0 butterfly per thread, shared-memory (not per-warp-region) exchange.
 template <typename T, int N1, int ALG>
@@ -811,7 +838,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   // strip's slots as before (coalesced W stores), j ^ 16 at lane ^ 8, and two even and
   // two odd team positions per warp (the padded exchange rows stay spread over the banks)
   const int slot = WCOL ? tid / GTT : tid % SLOTS;
-  const int j = WCOL ? tid % GTT : SHF2 ? (((tid >> 3) & 1) << 4) + ((tid >> 4) & 1) + ((tid >> 5) << 1) : tid / SLOTS;
+  const int j = WCOL ? tid % GTT : SHF2 ? shf2_team_pos(tid) : tid / SLOTS;
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);
 
@@ -1000,25 +1027,7 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
     if constexpr (SHF2) {
       ex.dep = LateDep{dep, dep_target, dep_seen, 1};  // checked at the (only) exchange's second barrier
       run_stages<N1, E, +1, 1, 16, 16>(v, j, tw1, 1, ex);
-      // v[i] = stage-2 output 256 (j >> 4) + (j & 15) + 16 i; butterfly jj = (j & 15) + 16 i
-      // pairs it with position jj + 256 (lane ^ 8, same i), twiddle w_512^jj. Lane h =
-      // j >> 4 takes the butterflies with i = 2c + h: jj = j + 32 c, outputs rows jj
-      // and jj + 256 — the layout line_fft returns (v[2c + i'] = row j + 32 c + 256 i').
-      const bool h = (j >> 4) != 0;
-      const C wj = __ldg(&tw1[j]);
-      Unroll<0, 8>::run([&](auto cc) {
-        constexpr int c = decltype(cc)::value;
-        const C snd = h ? v[2 * c] : v[2 * c + 1];
-        C rcv;
-        rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
-        rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
-        const C lo = h ? rcv : v[2 * c], hi = h ? v[2 * c + 1] : rcv;
-        constexpr T wc = (T)cos_2pi(c, 16), ws = (T)sin_2pi(c, 16);  // e^{2 pi i 32 c / 512}
-        const C w = c == 0 ? wj : cmul_cs(wj, wc, ws);
-        const C t = cmul(hi, w);
-        v[2 * c] = cadd(lo, t);
-        v[2 * c + 1] = csub(lo, t);
-      });
+      shf2_stage<T>(v, j, tw1);
     } else {
       if (has_ex) ex.dep = LateDep{dep, dep_target, dep_seen, 2 * (RCount<typename PL::R>::value - 1) - 1};
       line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});

@@ -56,6 +56,9 @@ GRFC_PLAN3(1024, double, 16, 2, 16, 16, 4)
 // columns {s CB + c}, {M - s CB - c} of a (j0, k1) row as one contiguous run at
 // s 2CB + side CB + c; pass B's column tiles work on positions (the axis-1 FFT does not
 // depend on which column it holds) and its row tiles load through wpos.
+#ifndef GRFC_SHF2_3D
+#define GRFC_SHF2_3D 1
+#endif
 #ifndef GRFC_WPERM3
 #define GRFC_WPERM3 1
 #endif
@@ -276,7 +279,9 @@ __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, SLOTS = 2 * PL::X, TT = N1 / E;
   constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
-  const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS;
+  // SHF2 (512-point columns): the final radix-2 stage on shuffles, as in the 2D column tile
+  constexpr bool SHF2 = col_shf2<N1, T>() && GRFC_SHF2_3D;
+  const int tid = threadIdx.x, slot = tid % SLOTS, j = SHF2 ? shf2_team_pos(tid) : tid / SLOTS;
   const int col = s * SLOTS + slot;
   C v[E];
   if (n1_per == N1) {
@@ -304,7 +309,12 @@ __device__ __forceinline__ void c2c_col_tile(const C_t<T>* __restrict__ src, int
   }
   std::conditional_t<col_padded<N1, T>(), ColExPad<C, SLOTS>, ColEx<C, SLOTS>> ex{reinterpret_cast<C*>(smem_raw), slot};
   if constexpr (HasTw16<decltype(ex)>::value) ex.tw16 = t16;
-  line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+  if constexpr (SHF2) {
+    run_stages<N1, E, +1, 1, 16, 16>(v, j, tw1, 1, ex);
+    shf2_stage<T>(v, j, tw1);
+  } else {
+    line_fft<N1, E, +1>(v, j, tw1, 1, ex, typename PL::R{});
+  }
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
