@@ -105,6 +105,8 @@ __device__ __forceinline__ void alg1_col_tile(const F2Params& p, int s, C_t<T>* 
   using PL = ColPlan<N1, T>;
   constexpr int E = PL::E, CB = PL::X, SLOTS = 2 * CB, TT = N1 / E;
   constexpr int R0 = RFirst<typename PL::R>::value, RL = RLast<typename PL::R>::value;
+  // (the shuffle final stage of the Algorithm-2 column tile, SHF2, measured slower here:
+  // 153 -> 147 Gpts/s at this kernel's 80 registers / 3 CTAs per SM)
   const int tid = threadIdx.x, slot = tid % SLOTS, j = tid / SLOTS, pslot = slot ^ CB;
   bool packed, mid;
   const int col = slot_column(s, slot, CB, p.m, packed, mid);

@@ -651,9 +651,9 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 __device__ __forceinline__ int shf2_team_pos(int tid) { return (((tid >> 3) & 1) << 4) + ((tid >> 4) & 1) + ((tid >> 5) << 1); }
 // After run_stages<512, 16, +1, 1, 16, 16>: v[i] = stage-2 output 256 (j >> 4) + (j & 15) + 16 i.
 // Butterfly jj = (j & 15) + 16 i pairs it with position jj + 256 (lane ^ 8, same i), twiddle
-// w_512^jj. Lane h = j >> 4 takes the butterflies with i = 2c + h: jj = j + 32 c, outputs rows
+// w_512^jj (the partner sits at lane ^ XOR). Lane h = j >> 4 takes the butterflies with i = 2c + h: jj = j + 32 c, outputs rows
 // jj and jj + 256 — the layout line_fft returns (v[2c + i'] = row j + 32 c + 256 i').
-template <typename T>
+template <typename T, int XOR = 8>
 __device__ __forceinline__ void shf2_stage(C_t<T>* v, int j, const C_t<T>* __restrict__ tw1) {
   using C = C_t<T>;
   const bool h = (j >> 4) != 0;
@@ -662,8 +662,8 @@ __device__ __forceinline__ void shf2_stage(C_t<T>* v, int j, const C_t<T>* __res
     constexpr int c = decltype(cc)::value;
     const C snd = h ? v[2 * c] : v[2 * c + 1];
     C rcv;
-    rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 8);
-    rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 8);
+    rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, XOR);
+    rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, XOR);
     const C lo = h ? rcv : v[2 * c], hi = h ? v[2 * c + 1] : rcv;
     constexpr T wc = (T)cos_2pi(c, 16), ws = (T)sin_2pi(c, 16);  // e^{2 pi i 32 c / 512}
     const C w = c == 0 ? wj : cmul_cs(wj, wc, ws);
