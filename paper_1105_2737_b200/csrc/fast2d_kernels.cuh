@@ -693,6 +693,18 @@ constexpr bool col_reggen_ok();
 #ifndef GRFC_SHF2
 #define GRFC_SHF2 1
 #endif
+// ZROW: the half-complex pre-twiddle Z[k] = (X[k] + conj X[M-k]) + i w_k (X[k] - conj X[M-k])
+// moves from the column tile's epilogue to the row tile's prologue, where a row team
+// (inside one warp) holds the whole row: the partner of element k = j + TT i sits in lane
+// TT - j, register E-1-i (lane 0: its own register E - i). Column tiles then own 2 CB
+// ADJACENT columns in natural order: W stores are one contiguous run per row and the row
+// loads one full line per half-warp (strip-blocked columns pay two half lines there).
+#ifndef GRFC_ZROW
+#define GRFC_ZROW 1
+#endif
+template <int N1, int M, typename T>
+constexpr bool zrow_ok();
+
 template <typename RS>
 struct IsR16_16_2 : std::false_type {};
 template <>
@@ -755,6 +767,12 @@ template <typename T, int N1, int MC, bool PERM = false>
 __device__ __forceinline__ void col_epilogue(const F2Params& p, int s, C_t<T>* __restrict__ Wf,
                                              const C_t<T>* __restrict__ tw2, C_t<T>* sm, C_t<T>* v, int slot, int j,
                                              int col, bool packed, bool mid);
+template <int N1, int M, typename T>
+constexpr bool zrow_ok() {
+  return GRFC_ZROW && sizeof(T) == 4 && !col_warp_mode<N1, T>() &&
+         RowPlan<M, T>::E == RFirst<typename RowPlan<M, T>::R>::value && M / RowPlan<M, T>::E <= 32 &&
+         32 % (M / RowPlan<M, T>::E) == 0 && RowPlan<M, T>::E % 2 == 0;
+}
 template <typename T, int N1, int ALG>
 constexpr bool col_reggen_ok() {
   return GRFC_REGGEN && (GRFC_REGGEN_WCOL || !col_warp_mode<N1, T>()) && sizeof(T) == 4 &&
@@ -814,7 +832,7 @@ struct NoHook {
 // `pre` runs on every thread after the column FFT and before the W stores (the
 // cluster scheduler waits there for the W slot to be free).
 template <typename T, int N1, int ALG, int MC = 0, typename Hook = NoHook, typename Pre = NoHook, bool PERM = false,
-          int DK = kDensAny, bool REGTILE = false>
+          int DK = kDensAny, bool REGTILE = false, bool ZROW = false>
 __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key, uint64_t fld, int s, C_t<T>* __restrict__ Wf,
                                          const C_t<T>* __restrict__ tw1, const C_t<T>* __restrict__ tw2,
                                          unsigned char* smem_raw, const float* __restrict__ rowq,
@@ -840,7 +858,12 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
   const int slot = WCOL ? tid / GTT : tid % SLOTS;
   const int j = WCOL ? tid % GTT : SHF2 ? shf2_team_pos(tid) : tid / SLOTS;
   bool packed, mid;
-  const int col = slot_column(s, slot, CB, p.m, packed, mid);
+  int col = slot_column(s, slot, CB, p.m, packed, mid);
+  if constexpr (ZROW) {  // 2 CB adjacent columns; column 0 is the packed (0, M) column
+    col = s * SLOTS + slot;
+    packed = col == 0;
+    mid = false;
+  }
 
   // Generation into shared memory (rolled loop: one copy of the Philox/Box-
   // Muller/density code in the I-cache). Thread j owns rows j + t*TT.
@@ -1039,7 +1062,19 @@ __device__ __forceinline__ void col_tile(const F2Params& p, const PhiloxKey& key
       __syncthreads();
     }
   }
-  col_epilogue<T, N1, MC, PERM>(p, s, Wf, tw2, sm, v, slot, j, col, packed, mid);
+  if constexpr (ZROW) {
+    // plain stores of the column transforms X (natural order, 2 CB adjacent columns)
+    static_assert(!WCOL, "ZROW: shared-exchange column plans only");
+    constexpr int RLz = RLast<typename PL::R>::value;
+    const int64_t mstride = MC > 0 ? (int64_t)MC : (int64_t)p.m;
+    C* __restrict__ wp = Wf + (int64_t)j * mstride + col;
+#pragma unroll
+    for (int b = 0; b < E / RLz; ++b)
+#pragma unroll
+      for (int i = 0; i < RLz; ++i) __stcg(wp + (b * TT + i * (N1 / RLz)) * mstride, v[b * RLz + i]);
+  } else {
+    col_epilogue<T, N1, MC, PERM>(p, s, Wf, tw2, sm, v, slot, j, col, packed, mid);
+  }
 }
 
 // Z epilogue + W stores of a column tile, lanes across the strip's slots
@@ -1127,7 +1162,7 @@ __device__ __forceinline__ void fused2d_row_table(const F2Params& p, float* rowq
 
 // Row tile: RPT consecutive rows (r0..) of one field — M-point exp(+) FFTs,
 // real field rows out. Block = RPT * (M/E) threads.
-template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook, int WPERM = 0>
+template <typename T, int M, int RPT, int NT = 0, typename Hook = NoHook, int WPERM = 0, bool ZROW = false>
 __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, int nrows, T* __restrict__ of,
                                          const C_t<T>* __restrict__ tw2, unsigned char* smem_raw,
                                          uint32_t* sig = nullptr, Hook hook = Hook{}, const C_t<T>* t16 = nullptr) {
@@ -1150,6 +1185,41 @@ __device__ __forceinline__ void row_tile(const C_t<T>* __restrict__ Wf, int r0, 
   // Release of the CTA's previous tile; its fence overlaps the W loads' latency.
   if (sig && threadIdx.x == 0) red_release_add(sig, 1u);
   if (threadIdx.x == 0) hook();
+  if constexpr (ZROW) {
+    // v[i] = X[k], k = j + TT i (column transforms, natural order). Registers are
+    // processed in pairs (lo = s, hi = E-1-s): lanes j >= 1 take X[M-k] from lane
+    // TT - j (its hi for our lo, its lo for our hi); lane 0 (k = TT i, partner TT (E - i))
+    // from its own registers E - s (the previous step's original hi) and s + 1;
+    // k = 0 is the packed (0, M) column, k = M/2 pairs with itself.
+    static_assert(E == R0 && WPERM == 0 && TT <= 32 && 32 % TT == 0 && E % 2 == 0, "ZROW geometry");
+    const int src = (TT - j) & (TT - 1);
+    const bool l0 = j == 0;
+    const C wj = __ldg(&tw2[j]);  // e^{2 pi i j / N2}; w_k = w_j e^{2 pi i TT i / N2}, TT i / N2 = i / (2 E)
+    C saved = v[0];
+    Unroll<0, E / 2>::run([&](auto ss) {
+      constexpr int st = decltype(ss)::value, lo = st, hi = E - 1 - st;
+      const C A = v[lo], B = v[hi];
+      C Pa, Pb;
+      Pa.x = __shfl_sync(0xffffffffu, B.x, src, TT);
+      Pa.y = __shfl_sync(0xffffffffu, B.y, src, TT);
+      Pb.x = __shfl_sync(0xffffffffu, A.x, src, TT);
+      Pb.y = __shfl_sync(0xffffffffu, A.y, src, TT);
+      const C own_b = v[st + 1];  // original: st + 1 <= hi is not overwritten yet
+      if (l0) {
+        Pa = saved;
+        Pb = own_b;
+      }
+      saved = B;
+      constexpr T ca = (T)cos_2pi(lo, 2 * E), sa = (T)sin_2pi(lo, 2 * E);
+      constexpr T cb = (T)cos_2pi(hi, 2 * E), sb = (T)sin_2pi(hi, 2 * E);
+      const C wa = lo == 0 ? wj : cmul_cs(wj, ca, sa), wb = cmul_cs(wj, cb, sb);
+      C Za = epilogue_z<T>(A, Pa, false, false, wa);
+      const C Zb = epilogue_z<T>(B, Pb, false, false, wb);
+      if (st == 0 && l0) Za = mk<C>(A.x + A.y, A.x - A.y);
+      v[lo] = Za;
+      v[hi] = Zb;
+    });
+  }
   // every team owns a row when the block holds exactly RPT teams (c2: 16 x 16 threads)
   constexpr bool ALL = NT == RPT * TT;
   constexpr bool WARP = GRFC_ROW_WARPSYNC && TT <= 32 && 32 % TT == 0;
@@ -1551,18 +1621,21 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), fused_min_blocks<N1
     // the previous tile's completion is released inside this one (see col_tile / row_tile)
     if (m.col) {
       // (a plan with a per-cell sqrt(g) table, p.sg, keeps the table path)
+      constexpr bool ZR = ALG == GRFC_ONE_FFT_OVERWRITE && zrow_ok<N1, M, T>();
+      constexpr bool PM = !ZR && w_perm_cb<N1, T>() > 0;
       if (col_reggen_ok<T, N1, ALG>() && table && !p.sg && m.idx > 0)
-        col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK, col_reggen_ok<T, N1, ALG>()>(
+        col_tile<T, N1, ALG, M, decltype(hook), NoHook, PM, DK, col_reggen_ok<T, N1, ALG>(), ZR>(
             p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw, s_rowq,
             GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT, done_ctr, hook, t16);
       else
-        col_tile<T, N1, ALG, M, decltype(hook), NoHook, (w_perm_cb<N1, T>() > 0), DK>(
+        col_tile<T, N1, ALG, M, decltype(hook), NoHook, PM, DK, false, ZR>(
             p, key, field0 + foff + (uint64_t)m.f * fstep, (int)m.idx, Wf, tw1, tw2, smem_raw,
             table ? s_rowq : nullptr, GRFC_COL_LATE_WAIT && m.use ? &q.row_done[m.slot] : nullptr, m.use * RT,
             done_ctr, hook, t16);
       done_ctr = &q.col_done[m.slot];
     } else {
-      row_tile<T, M, RPT, fused_threads<N1, M, T>(), decltype(hook), w_perm_cb<N1, T>()>(
+      constexpr bool ZR = ALG == GRFC_ONE_FFT_OVERWRITE && zrow_ok<N1, M, T>();
+      row_tile<T, M, RPT, fused_threads<N1, M, T>(), decltype(hook), ZR ? 0 : w_perm_cb<N1, T>(), ZR>(
           Wf, (int)m.idx * RPT, N1, out + (int64_t)(foff + (uint64_t)m.f * fstep) * out_stride, tw2, smem_raw,
           done_ctr, hook, t16);
       done_ctr = &q.row_done[m.slot];
@@ -1735,7 +1808,8 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), cl_min_blocks<N1, M
       // (the arrive after its rows); the first column tile waits for that just
       // before its W stores, so the barrier's latency hides behind its FFT.
       const ClusterWaitPre pre{NSL == 1 && first && it > 0};
-      col_tile<T, N1, GRFC_ONE_FFT_OVERWRITE, M, NoHook, ClusterWaitPre, (w_perm_cb<N1, T>() > 0)>(
+      col_tile<T, N1, GRFC_ONE_FFT_OVERWRITE, M, NoHook, ClusterWaitPre, (!zrow_ok<N1, M, T>() && w_perm_cb<N1, T>() > 0),
+               kDensAny, false, zrow_ok<N1, M, T>()>(
           p, key, field0 + f, (int)sidx, Wf, tw1, tw2, smem_raw, table ? s_rowq : nullptr, nullptr, 0, nullptr,
           NoHook{}, t16, pre);
       first = false;
@@ -1745,7 +1819,7 @@ __global__ void __launch_bounds__(fused_threads<N1, M, T>(), cl_min_blocks<N1, M
     cluster_arrive();
     cluster_wait();
     for (uint32_t r = rank; r < RT; r += cs) {
-      row_tile<T, M, RPT, NT, NoHook, w_perm_cb<N1, T>()>(Wf, (int)r * RPT, N1, out + (int64_t)f * out_stride, tw2,
+      row_tile<T, M, RPT, NT, NoHook, (zrow_ok<N1, M, T>() ? 0 : w_perm_cb<N1, T>()), zrow_ok<N1, M, T>()>(Wf, (int)r * RPT, N1, out + (int64_t)f * out_stride, tw2,
                                                            smem_raw, nullptr, NoHook{},
                               t16);
       __syncthreads();
