@@ -1,3 +1,8 @@
+#!/bin/bash
+# Deferral-schedule sweep (measurement 4). Needs a library built with
+#   make -C paper_1105_2737_b200 build/libgrfc_xdefer.so XDEFS=-DGRFC_DEFER_BUILD=15
+# and GRFC_LIB=paper_1105_2737_b200/build/libgrfc_xdefer.so: checks bit-identity against the
+# default schedule on 1/40/300 fields, then sweeps the ring geometry on c2, c5 and c3.
 cd /root/repo
 cat > /tmp/t.py <<'PY'
 import os, sys, torch

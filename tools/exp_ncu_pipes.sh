@@ -1,3 +1,6 @@
+#!/bin/bash
+# Pipe utilisation of the c2 kernel (ncu sections + the L1/shared data-pipe wavefront metric
+# that DESIGN.md 8 builds on).
 cd /root/repo
 cat > /tmp/r.py <<'PY'
 import os, sys, torch
